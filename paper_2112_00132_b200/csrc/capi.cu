@@ -1,0 +1,681 @@
+// capi.cu — the C ABI of libatos.so (include/atos.h): graph handles,
+// workspaces, the persistent / discrete / BSP drivers for BFS, PageRank and
+// colouring, timing and statistics.  Every function returns atos_status and
+// records a detail string on error; nothing here aborts the process.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+
+#include "../../include/atos.h"
+#include "kernels.cuh"
+#include "capi_internal.h"
+
+using namespace atos;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+atos_status atos_set_error(atos_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define CK(call)                                                                                          \
+  do {                                                                                                    \
+    cudaError_t e_ = (call);                                                                              \
+    if (e_ != cudaSuccess) {                                                                              \
+      (void)cudaGetLastError();                                                                           \
+      return atos_set_error(e_ == cudaErrorMemoryAllocation ? ATOS_ERR_OUT_OF_MEMORY : ATOS_ERR_CUDA,   \
+                            "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));           \
+    }                                                                                                     \
+  } while (0)
+
+#define CKS(call)                        \
+  do {                                   \
+    atos_status s_ = (call);             \
+    if (s_ != ATOS_OK) return s_;        \
+  } while (0)
+
+extern "C" const char* atos_status_string(atos_status s) {
+  switch (s) {
+    case ATOS_OK: return "ATOS_OK";
+    case ATOS_ERR_INVALID_ARGUMENT: return "ATOS_ERR_INVALID_ARGUMENT";
+    case ATOS_ERR_INVALID_GRAPH: return "ATOS_ERR_INVALID_GRAPH";
+    case ATOS_ERR_OUT_OF_MEMORY: return "ATOS_ERR_OUT_OF_MEMORY";
+    case ATOS_ERR_CUDA: return "ATOS_ERR_CUDA";
+    case ATOS_ERR_NCCL: return "ATOS_ERR_NCCL";
+    case ATOS_ERR_QUEUE_OVERFLOW: return "ATOS_ERR_QUEUE_OVERFLOW";
+    case ATOS_ERR_TIMEOUT: return "ATOS_ERR_TIMEOUT";
+    case ATOS_ERR_UNSUPPORTED: return "ATOS_ERR_UNSUPPORTED";
+  }
+  return "ATOS_ERR_UNKNOWN";
+}
+extern "C" const char* atos_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* atos_version(void) { return "atos-b200 1.0 sm_100a"; }
+
+extern "C" void atos_config_default(atos_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof *c);
+  c->struct_size = sizeof(atos_config);
+  c->kernel = ATOS_KERNEL_PERSISTENT;
+  c->worker = ATOS_WORKER_CTA;
+  c->cta_threads = 256;
+  c->fetch_size = 256;
+  c->num_blocks = 0;
+  c->bfs_filter = 1;
+  c->pr_activation = 0;
+  c->check_size = 32;
+  c->gc_literal = 0;
+  c->queue_capacity = 0;
+  c->timeout_s = 0.0;
+  c->stream = nullptr;
+}
+
+static atos_status check_config(const atos_config* c) {
+  if (c->struct_size != sizeof(atos_config))
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "atos_config.struct_size %u != %zu (use atos_config_default)",
+                          c->struct_size, sizeof(atos_config));
+  if (c->kernel < 0 || c->kernel > 2) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "bad kernel %d", c->kernel);
+  if (c->worker < 0 || c->worker > 2) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "bad worker %d", c->worker);
+  if (c->cta_threads < 32 || c->cta_threads > 1024 || c->cta_threads % 32)
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "cta_threads %d not a multiple of 32 in [32,1024]", c->cta_threads);
+  if (c->fetch_size < 1 || c->fetch_size > (1 << 16))
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d not in [1, 65536]", c->fetch_size);
+  if (c->num_blocks < 0) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "num_blocks < 0");
+  if (c->queue_capacity < 0) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "queue_capacity < 0");
+  if (!(c->timeout_s >= 0)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "timeout_s < 0");
+  if (c->pr_activation != 0 && c->pr_activation != 1)
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "pr_activation must be 0 or 1");
+  if (c->pr_activation == 1 && c->check_size < 1)
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "check_size < 1");
+  return ATOS_OK;
+}
+
+// ------------------------------------------------------------------ graph
+__global__ void k_validate(const int64_t* off, const int32_t* col, int64_t n, int64_t m, unsigned int* bad) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = tid; v < n; v += stride)
+    if (off[v + 1] < off[v]) atomicOr(bad, 1u);
+  for (int64_t e = tid; e < m; e += stride)
+    if (col[e] < 0 || (int64_t)col[e] >= n) atomicOr(bad, 2u);
+  if (tid == 0 && (off[0] != 0 || off[n] != m)) atomicOr(bad, 4u);
+}
+__global__ void k_max_degree(const int64_t* off, int64_t n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(off[v + 1] - off[v]));
+  for (int d = 16; d; d >>= 1) m = max(m, __shfl_xor_sync(FULL_MASK, m, d));
+  if (lane_id() == 0) atomicMax(out, m);
+}
+
+static int grid_for(int64_t work, int threads, int sms) {
+  int64_t b = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)sms * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+static atos_status device_sms(int* sms) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+  return ATOS_OK;
+}
+
+atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* col, int64_t n, int64_t m,
+                              uint32_t flags) {
+  g->n = n;
+  g->m = m;
+  g->symmetric = (flags & ATOS_GRAPH_SYMMETRIC) != 0;
+  CK(cudaGetDevice(&g->device));
+  CKS(device_sms(&g->sms));
+  const bool dev_ptrs = flags & ATOS_GRAPH_DEVICE_PTRS;
+  const bool borrow = dev_ptrs && (flags & ATOS_GRAPH_BORROW) && (((uintptr_t)col & 15) == 0);
+  if (borrow) {
+    g->d_off = const_cast<int64_t*>(off);
+    g->d_col = const_cast<int32_t*>(col);
+    g->owned = false;
+  } else {
+    CK(cudaMalloc(&g->d_off, (size_t)(n + 1) * sizeof(int64_t)));
+    CK(cudaMalloc(&g->d_col, (size_t)std::max<int64_t>(m, 4) * sizeof(int32_t)));
+    g->owned = true;
+    CK(cudaMemcpy(g->d_off, off, (size_t)(n + 1) * sizeof(int64_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
+    if (m) CK(cudaMemcpy(g->d_col, col, (size_t)m * sizeof(int32_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
+  }
+  CK(cudaMalloc(&g->d_scratch, 256));
+  CK(cudaMemset(g->d_scratch, 0, 256));
+  if (flags & ATOS_GRAPH_VALIDATE) {
+    unsigned int* bad = reinterpret_cast<unsigned int*>(g->d_scratch);
+    k_validate<<<grid_for(std::max(n, m), 256, g->sms), 256>>>(g->d_off, g->d_col, n, m, bad);
+    unsigned int hbad = 0;
+    CK(cudaMemcpy(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost));
+    if (hbad)
+      return atos_set_error(ATOS_ERR_INVALID_GRAPH, "CSR validation failed (code %u: 1=non-monotone offsets, "
+                            "2=column out of range, 4=off[0]!=0 or off[n]!=m)", hbad);
+  }
+  unsigned long long* md = reinterpret_cast<unsigned long long*>(g->d_scratch) + 2;
+  if (n) k_max_degree<<<grid_for(n, 256, g->sms), 256>>>(g->d_off, n, md);
+  unsigned long long hmd = 0;
+  CK(cudaMemcpy(&hmd, md, sizeof hmd, cudaMemcpyDeviceToHost));
+  g->max_degree = (int64_t)hmd;
+  CK(cudaDeviceSynchronize());
+  return ATOS_OK;
+}
+
+static void graph_free(atos_graph g) {
+  if (!g) return;
+  if (g->owned) {
+    cudaFree(g->d_off);
+    cudaFree(g->d_col);
+  }
+  cudaFree(g->d_scratch);
+  Workspace& w = g->ws;
+  cudaFree(w.ring);
+  cudaFree(w.ctl);
+  cudaFree(w.u32a);
+  cudaFree(w.f32a);
+  cudaFree(w.f32b);
+  cudaFree(w.front[0]);
+  cudaFree(w.front[1]);
+  cudaFree(w.fcount);
+  if (w.h_ctl) cudaFreeHost(w.h_ctl);
+  for (auto& e : w.ev)
+    if (e) cudaEventDestroy(e);
+  dist_free(g);
+  delete g;
+}
+
+extern "C" atos_status atos_graph_create(const int64_t* off, const int32_t* col, int64_t n, int64_t m, uint32_t flags,
+                                         atos_graph* out) {
+  if (!out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "out == NULL");
+  *out = nullptr;
+  if (n < 0 || m < 0) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "n < 0 or m < 0");
+  if (!off || (m > 0 && !col)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "NULL CSR pointer");
+  if (n >= 0x7FFFFFFFLL) return atos_set_error(ATOS_ERR_UNSUPPORTED, "n >= 2^31-1 (bit 31 tags colouring tasks)");
+  atos_graph g = new (std::nothrow) atos_graph_s();
+  if (!g) return atos_set_error(ATOS_ERR_OUT_OF_MEMORY, "host allocation");
+  atos_status s = graph_init_common(g, off, col, n, m, flags);
+  if (s != ATOS_OK) {
+    graph_free(g);
+    return s;
+  }
+  *out = g;
+  return ATOS_OK;
+}
+
+extern "C" atos_status atos_graph_destroy(atos_graph g) {
+  if (!g) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "NULL graph");
+  graph_free(g);
+  return ATOS_OK;
+}
+
+extern "C" atos_status atos_graph_info(atos_graph g, int64_t* n, int64_t* m, int64_t* maxd) {
+  if (!g) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "NULL graph");
+  if (n) *n = g->global_n ? g->global_n : g->n;
+  if (m) *m = g->m;
+  if (maxd) *maxd = g->max_degree;
+  return ATOS_OK;
+}
+
+// ------------------------------------------------------------------ workspace
+template <class T>
+static atos_status ensure(T*& p, size_t& have, size_t want_elems) {
+  if (p && have >= want_elems) return ATOS_OK;
+  cudaFree(p);
+  p = nullptr;
+  have = 0;
+  CK(cudaMalloc(&p, std::max<size_t>(want_elems, 1) * sizeof(T)));
+  have = want_elems;
+  return ATOS_OK;
+}
+
+static uint64_t pow2_at_least(uint64_t x, uint64_t floor_cap = 1024) {
+  uint64_t c = floor_cap;
+  while (c < x) c <<= 1;
+  return c;
+}
+
+atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, uint64_t default_cap, bool need_ring,
+                       cudaStream_t s) {
+  Workspace& w = g->ws;
+  if (!w.ctl) {
+    CK(cudaMalloc(&w.ctl, sizeof(QueueCtl)));
+    CK(cudaMallocHost(&w.h_ctl, sizeof(QueueCtl)));
+    for (auto& e : w.ev) CK(cudaEventCreate(&e));
+    CK(cudaMalloc(&w.fcount, 4 * sizeof(unsigned long long)));
+  }
+  if (need_ring) {
+    uint64_t cap = cfg.queue_capacity > 0 ? pow2_at_least((uint64_t)cfg.queue_capacity, 32) : pow2_at_least(default_cap);
+    if (cap != w.cap) {
+      cudaFree(w.ring);
+      w.ring = nullptr;
+      CK(cudaMalloc(&w.ring, cap * sizeof(uint64_t)));
+      CK(cudaMemsetAsync(w.ring, 0, cap * sizeof(uint64_t), s));
+      w.cap = cap;
+      w.dirty = 0;
+    } else if (w.dirty) {
+      CK(cudaMemsetAsync(w.ring, 0, std::min<uint64_t>(w.dirty, cap) * sizeof(uint64_t), s));
+      w.dirty = 0;
+    }
+  }
+  (void)n_local;
+  return ATOS_OK;
+}
+
+static Queue make_queue(atos_graph g, const atos_config& cfg) {
+  Queue q{};
+  q.ring = g->ws.ring;
+  q.mask = g->ws.cap - 1;
+  q.log2cap = 0;
+  while ((1ull << q.log2cap) < g->ws.cap) q.log2cap++;
+  q.ctl = g->ws.ctl;
+  q.deadline = 0;
+  q.timeout_ns = cfg.timeout_s > 0 ? (uint64_t)(cfg.timeout_s * 1e9) : 0;
+  q.head_floor = 0;
+  return q;
+}
+
+// Read back the control block; translate abort codes.
+static atos_status read_ctl(atos_graph g, cudaStream_t s) {
+  CK(cudaMemcpyAsync(g->ws.h_ctl, g->ws.ctl, sizeof(QueueCtl), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t ab = g->ws.h_ctl->abort.v;
+  if (ab == ABORT_OVERFLOW)
+    return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "task queue overflow (capacity %llu); retry with a larger "
+                          "queue_capacity", (unsigned long long)g->ws.cap);
+  if (ab == ABORT_TIMEOUT) return atos_set_error(ATOS_ERR_TIMEOUT, "device watchdog fired");
+  if (ab) return atos_set_error(ATOS_ERR_CUDA, "unknown abort code %llu", (unsigned long long)ab);
+  return ATOS_OK;
+}
+
+// ------------------------------------------------------------------ launchers
+struct LaunchCtx {
+  atos_graph g;
+  atos_config cfg;
+  cudaStream_t s;
+  GraphView gv;
+  int64_t launches = 0;
+  int64_t rounds = 0;
+  std::chrono::steady_clock::time_point t0;
+};
+
+template <class K>
+static atos_status set_smem(K kern, size_t smem) {
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return ATOS_OK;
+}
+
+template <class P, class App, int W>
+static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q) {
+  auto kern = k_persistent<P, App, W>;
+  const int F = c.cfg.fetch_size, T = c.cfg.cta_threads;
+  const size_t smem = (W == W_CTA) ? P::smem_bytes(F) : 0;
+  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d needs %zu B smem", F, smem);
+  CKS(set_smem(kern, smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
+  if (per_sm < 1) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "kernel cannot be resident with %d threads", T);
+  int blocks = per_sm * c.g->sms;
+  if (c.cfg.num_blocks > 0) blocks = std::min(blocks, c.cfg.num_blocks);  // persistent: <= resident maximum
+  kern<<<blocks, T, smem, c.s>>>(app, c.gv, q, F);
+  CK(cudaGetLastError());
+  c.launches++;
+  return ATOS_OK;
+}
+
+template <class P, class App>
+static atos_status run_persistent(LaunchCtx& c, const App& app, const Queue& q) {
+  switch (c.cfg.worker) {
+    case ATOS_WORKER_THREAD: return run_persistent_w<P, App, W_THREAD>(c, app, q);
+    case ATOS_WORKER_WARP: return run_persistent_w<P, App, W_WARP>(c, app, q);
+    default: return run_persistent_w<P, App, W_CTA>(c, app, q);
+  }
+}
+
+static atos_status host_timeout(LaunchCtx& c) {
+  if (c.cfg.timeout_s > 0) {
+    double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - c.t0).count();
+    if (el > c.cfg.timeout_s) return atos_set_error(ATOS_ERR_TIMEOUT, "host watchdog: %.1f s", el);
+  }
+  return ATOS_OK;
+}
+
+// Discrete scheduler: one launch per round over the queue snapshot [h, t).
+template <class P, class App, int W>
+static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0) {
+  auto kern = k_discrete<P, App, W>;
+  const int F = c.cfg.fetch_size, T = c.cfg.cta_threads;
+  const size_t smem = (W == W_CTA) ? P::smem_bytes(F) : 0;
+  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d needs %zu B smem", F, smem);
+  CKS(set_smem(kern, smem));
+  const uint64_t chunk = (W == W_CTA) ? (uint64_t)F : (W == W_WARP ? (uint64_t)F : 32ull * (uint64_t)F);
+  const uint64_t per_block = (W == W_CTA) ? 1 : (uint64_t)(T / 32);
+  uint64_t h = 0, t = t0;
+  uint64_t* h_tail = &c.g->ws.h_ctl->tail.v;
+  while (h < t) {
+    const uint64_t workers = (t - h + chunk - 1) / chunk;
+    uint64_t blocks = (workers + per_block - 1) / per_block;
+    blocks = std::min<uint64_t>(blocks, 1u << 30);
+    q.head_floor = t;
+    kern<<<(unsigned)blocks, T, smem, c.s>>>(app, c.gv, q, h, t, F);
+    CK(cudaGetLastError());
+    c.launches++;
+    c.rounds++;
+    // one device->host crossing per round: the new tail and the abort flag
+    CK(cudaMemcpyAsync(h_tail, &c.g->ws.ctl->tail.v, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+    CK(cudaMemcpyAsync(&c.g->ws.h_ctl->abort.v, &c.g->ws.ctl->abort.v, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+    CK(cudaStreamSynchronize(c.s));
+    if (c.g->ws.h_ctl->abort.v) break;
+    CKS(host_timeout(c));
+    h = t;
+    t = *h_tail;
+  }
+  return ATOS_OK;
+}
+
+template <class P, class App>
+static atos_status run_discrete(LaunchCtx& c, const App& app, const Queue& q, uint64_t t0) {
+  switch (c.cfg.worker) {
+    case ATOS_WORKER_THREAD: return run_discrete_w<P, App, W_THREAD>(c, app, q, t0);
+    case ATOS_WORKER_WARP: return run_discrete_w<P, App, W_WARP>(c, app, q, t0);
+    default: return run_discrete_w<P, App, W_CTA>(c, app, q, t0);
+  }
+}
+
+// One BSP step over an explicit frontier (in == nullptr: all vertices).
+template <class P, class App, int W>
+static atos_status bsp_step_w(LaunchCtx& c, const App& app, const uint32_t* in, uint64_t count, uint32_t* out,
+                              unsigned long long* out_count, int F, QueueCtl* ctl) {
+  if (count == 0) return ATOS_OK;
+  auto kern = k_bsp<P, App, W>;
+  const int T = c.cfg.cta_threads;
+  const size_t smem = (W == W_CTA) ? P::smem_bytes(F) : 0;
+  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d needs %zu B smem", F, smem);
+  CKS(set_smem(kern, smem));
+  const uint64_t chunk = (W == W_CTA) ? (uint64_t)F : (W == W_WARP ? (uint64_t)F : 32ull * (uint64_t)F);
+  const uint64_t per_block = (W == W_CTA) ? 1 : (uint64_t)(T / 32);
+  const uint64_t workers = (count + chunk - 1) / chunk;
+  uint64_t blocks = std::min<uint64_t>((workers + per_block - 1) / per_block, 1u << 30);
+  kern<<<(unsigned)blocks, T, smem, c.s>>>(app, c.gv, in, count, out, out_count, ctl, F);
+  CK(cudaGetLastError());
+  c.launches++;
+  return ATOS_OK;
+}
+
+template <class P, class App>
+static atos_status bsp_step(LaunchCtx& c, const App& app, const uint32_t* in, uint64_t count, uint32_t* out,
+                            unsigned long long* out_count) {
+  const int F = c.cfg.fetch_size;
+  switch (c.cfg.worker) {
+    case ATOS_WORKER_THREAD: return bsp_step_w<P, App, W_THREAD>(c, app, in, count, out, out_count, F, c.g->ws.ctl);
+    case ATOS_WORKER_WARP: return bsp_step_w<P, App, W_WARP>(c, app, in, count, out, out_count, F, c.g->ws.ctl);
+    default: return bsp_step_w<P, App, W_CTA>(c, app, in, count, out, out_count, F, c.g->ws.ctl);
+  }
+}
+
+static atos_status bsp_read_count(LaunchCtx& c, unsigned long long* dcount, uint64_t& out) {
+  CK(cudaMemcpyAsync(&c.g->ws.h_ctl->aux[3].v, dcount, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+  CK(cudaStreamSynchronize(c.s));
+  out = c.g->ws.h_ctl->aux[3].v;
+  c.rounds++;
+  return host_timeout(c);
+}
+
+static int fill_blocks(int64_t n, int sms) { return grid_for(n, 256, sms); }
+
+// Output copy: host or device destination (UVA).
+static atos_status copy_out(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return ATOS_OK;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+  return ATOS_OK;
+}
+
+static atos_status finish_stats(LaunchCtx& c, atos_stats* st, bool bsp) {
+  Workspace& w = c.g->ws;
+  CK(cudaEventRecord(w.ev[2], c.s));
+  CKS(read_ctl(c.g, c.s));
+  if (!bsp) w.dirty = std::max<uint64_t>(w.dirty, std::min<uint64_t>(w.h_ctl->tail.v, w.cap));
+  if (st) {
+    float ms = 0, kms = 0;
+    CK(cudaEventElapsedTime(&ms, w.ev[0], w.ev[2]));
+    CK(cudaEventElapsedTime(&kms, w.ev[1], w.ev[2]));
+    st->ms = ms;
+    st->kernel_ms = kms;
+    st->kernel_launches = c.launches;
+    st->tasks_popped = (int64_t)w.h_ctl->stats[0].v;
+    st->tasks_pushed = (int64_t)w.h_ctl->stats[1].v;
+    st->edges_processed = (int64_t)w.h_ctl->stats[2].v;
+    st->rounds = c.rounds;
+    st->queue_high_water = bsp ? (int64_t)w.h_ctl->high_water.v : (int64_t)w.h_ctl->high_water.v;
+  }
+  return ATOS_OK;
+}
+
+static atos_status begin_call(atos_graph g, const atos_config* cfg_in, LaunchCtx& c, atos_stats* st) {
+  if (!g) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "NULL graph");
+  if (cfg_in) c.cfg = *cfg_in;
+  else atos_config_default(&c.cfg);
+  CKS(check_config(&c.cfg));
+  if (st) {
+    if (st->struct_size != 0 && st->struct_size != sizeof(atos_stats))
+      return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "atos_stats.struct_size mismatch");
+    std::memset(st, 0, sizeof *st);
+    st->struct_size = sizeof(atos_stats);
+  }
+  c.g = g;
+  c.s = reinterpret_cast<cudaStream_t>(c.cfg.stream);
+  c.gv = GraphView{g->d_off, g->d_col, g->n};
+  c.t0 = std::chrono::steady_clock::now();
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev != g->device) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "current device %d != graph device %d", dev, g->device);
+  return ATOS_OK;
+}
+
+// ------------------------------------------------------------------ BFS
+atos_status bfs_local(LaunchCtx& c, int64_t src, const atos_config& cfg);
+
+extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t* depth_out, atos_stats* st) {
+  LaunchCtx c;
+  CKS(begin_call(g, cfg, c, st));
+  if (g->comm) return dist_bfs(g, src, &c.cfg, depth_out, st);
+  const int64_t n = g->n;
+  if (n == 0) return ATOS_OK;
+  if (src < 0 || src >= n) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "src %lld not in [0, %lld)", (long long)src, (long long)n);
+  if (!depth_out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "depth_out == NULL");
+  Workspace& w = g->ws;
+  const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
+  CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)n, !bsp, c.s));
+  CKS(ensure(w.u32a, w.u32a_n, (size_t)n));
+  if (bsp) {
+    CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
+    CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
+  }
+  CK(cudaEventRecord(w.ev[0], c.s));
+  // a2: init (timed)
+  k_bfs_init<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, n, src);
+  k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : 1, w.ring, bsp ? -1 : src);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(w.ev[1], c.s));
+  BfsApp app{w.u32a, c.cfg.bfs_filter};
+  using P = EdgeMapPolicy<BfsApp>;
+  if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
+    CKS(run_persistent<P>(c, app, make_queue(g, c.cfg)));
+  } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
+    CKS(run_discrete<P>(c, app, make_queue(g, c.cfg), 1));
+  } else {
+    // Alg. 1: double-buffered frontiers
+    uint32_t h_src = (uint32_t)src;
+    CK(cudaMemcpyAsync(w.front[0], &h_src, sizeof h_src, cudaMemcpyHostToDevice, c.s));
+    uint64_t cnt = 1;
+    int cur = 0;
+    while (cnt > 0) {
+      CK(cudaMemsetAsync(w.fcount, 0, sizeof(unsigned long long), c.s));
+      CKS(bsp_step<P>(c, app, w.front[cur], cnt, w.front[cur ^ 1], w.fcount));
+      CKS(bsp_read_count(c, w.fcount, cnt));
+      cur ^= 1;
+    }
+  }
+  CKS(finish_stats(c, st, bsp));
+  CKS(copy_out(depth_out, w.u32a, (size_t)n * sizeof(uint32_t), c.s));
+  CK(cudaStreamSynchronize(c.s));
+  return ATOS_OK;
+}
+
+// ------------------------------------------------------------------ PageRank
+extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const atos_config* cfg, float* rank_out,
+                                     atos_stats* st) {
+  LaunchCtx c;
+  CKS(begin_call(g, cfg, c, st));
+  if (!(alpha > 0.f && alpha < 1.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "alpha not in (0,1)");
+  if (!(eps > 0.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "eps <= 0 or NaN");
+  if (g->comm) return dist_pagerank(g, alpha, eps, &c.cfg, rank_out, st);
+  const int64_t n = g->n;
+  if (n == 0) return ATOS_OK;
+  if (!rank_out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "rank_out == NULL");
+  if (c.cfg.pr_activation == 1) return atos_set_error(ATOS_ERR_UNSUPPORTED, "Check_Size window activation not built");
+  Workspace& w = g->ws;
+  const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
+  // at most 2 live copies per vertex (initial + one threshold crossing)
+  CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)n, !bsp, c.s));
+  CKS(ensure(w.f32a, w.f32a_n, (size_t)n));
+  CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
+  if (bsp) {
+    CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
+    CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
+  }
+  if (!bsp && (uint64_t)n > w.cap)
+    return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "queue_capacity %llu < n = %lld initial tasks",
+                          (unsigned long long)w.cap, (long long)n);
+  float* rank = w.f32a;
+  float* res = w.f32b;
+  CK(cudaEventRecord(w.ev[0], c.s));
+  // a2: rank = 1 - alpha ; residue seeded by one synchronous push (R4) ; all vertices enqueued
+  k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rank, n, 1.0f - alpha);
+  k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, 0.0f);
+  k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
+  {
+    PrInitApp ia{res, (1.0f - alpha) * alpha};
+    atos_config ic = c.cfg;
+    ic.worker = ATOS_WORKER_CTA;
+    LaunchCtx ci = c;
+    ci.cfg = ic;
+    CKS((bsp_step_w<EdgeMapPolicy<PrInitApp>, PrInitApp, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr, nullptr, 256, nullptr)));
+  }
+  if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(w.ev[1], c.s));
+  PrApp app{rank, res, alpha, eps};
+  if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
+    CKS(run_persistent<EdgeMapPolicy<PrApp>>(c, app, make_queue(g, c.cfg)));
+  } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
+    CKS(run_discrete<EdgeMapPolicy<PrApp>>(c, app, make_queue(g, c.cfg), (uint64_t)n));
+  } else {
+    // Alg. 3: push kernel over the frontier, then filter kernel over all vertices
+    PrBspApp bapp{app};
+    uint64_t cnt = (uint64_t)n;
+    const uint32_t* in = nullptr;  // first frontier: all vertices
+    int cur = 0;
+    while (cnt > 0) {
+      CKS(bsp_step<EdgeMapPolicy<PrBspApp>>(c, bapp, in, cnt, nullptr, nullptr));
+      CK(cudaMemsetAsync(w.fcount, 0, sizeof(unsigned long long), c.s));
+      k_pr_filter<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, eps, w.front[cur], w.fcount);
+      CK(cudaGetLastError());
+      c.launches++;
+      CKS(bsp_read_count(c, w.fcount, cnt));
+      in = w.front[cur];
+      cur ^= 1;
+    }
+  }
+  CKS(finish_stats(c, st, bsp));
+  if (st) {
+    unsigned int* mb = reinterpret_cast<unsigned int*>(g->d_scratch) + 8;
+    CK(cudaMemsetAsync(mb, 0, sizeof(unsigned int), c.s));
+    k_max_f32<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, mb);
+    unsigned int hb = 0;
+    CK(cudaMemcpyAsync(&hb, mb, sizeof hb, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaStreamSynchronize(c.s));
+    float f;
+    std::memcpy(&f, &hb, sizeof f);
+    st->max_residue = f;
+  }
+  CKS(copy_out(rank_out, rank, (size_t)n * sizeof(float), c.s));
+  CK(cudaStreamSynchronize(c.s));
+  return ATOS_OK;
+}
+
+// ------------------------------------------------------------------ colouring
+extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t* color_out, int32_t* ncolors_out,
+                                  atos_stats* st) {
+  LaunchCtx c;
+  CKS(begin_call(g, cfg, c, st));
+  if (g->comm) return atos_set_error(ATOS_ERR_UNSUPPORTED, "colouring is single-GPU (SURVEY §8e: replicas only)");
+  if (!g->symmetric) return atos_set_error(ATOS_ERR_INVALID_GRAPH, "atos_color needs ATOS_GRAPH_SYMMETRIC");
+  if (c.cfg.gc_literal) return atos_set_error(ATOS_ERR_UNSUPPORTED, "paper-literal colouring (livelocks, R13) not built");
+  const int64_t n = g->n;
+  if (ncolors_out) *ncolors_out = 0;
+  if (n == 0) return ATOS_OK;
+  if (!color_out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "color_out == NULL");
+  Workspace& w = g->ws;
+  const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
+  CKS(ws_prepare(g, c.cfg, n, 4 * (uint64_t)n, !bsp, c.s));
+  CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // pend flags
+  CKS(ensure(reinterpret_cast<float*&>(w.f32a), w.f32a_n, (size_t)n));
+  int32_t* color = reinterpret_cast<int32_t*>(w.f32a);
+  uint32_t* pend = w.u32a;
+  if (!bsp && (uint64_t)n > w.cap)
+    return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "queue_capacity %llu < n = %lld initial tasks",
+                          (unsigned long long)w.cap, (long long)n);
+  if (bsp) {
+    CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
+    CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
+  }
+  CK(cudaEventRecord(w.ev[0], c.s));
+  k_fill<int32_t><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(color, n, -1);
+  k_fill<uint32_t><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(pend, n, 1u);
+  k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
+  if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);  // ASSIGN(v), id order (R22)
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(w.ev[1], c.s));
+  GcApp app{color, pend};
+  if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
+    CKS(run_persistent<GcPolicy<GC_UBER>>(c, app, make_queue(g, c.cfg)));
+  } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
+    CKS(run_discrete<GcPolicy<GC_UBER>>(c, app, make_queue(g, c.cfg), (uint64_t)n));
+  } else {
+    // Alg. 5: assign kernel then conflict-detect kernel over the frontier
+    uint64_t cnt = (uint64_t)n;
+    const uint32_t* in = nullptr;
+    int cur = 0;
+    while (cnt > 0) {
+      CKS(bsp_step<GcPolicy<GC_BSP_ASSIGN>>(c, app, in, cnt, nullptr, nullptr));
+      CK(cudaMemsetAsync(w.fcount, 0, sizeof(unsigned long long), c.s));
+      CKS(bsp_step<GcPolicy<GC_BSP_DETECT>>(c, app, in, cnt, w.front[cur], w.fcount));
+      CKS(bsp_read_count(c, w.fcount, cnt));
+      in = w.front[cur];
+      cur ^= 1;
+    }
+  }
+  CKS(finish_stats(c, st, bsp));
+  int* mx = reinterpret_cast<int*>(g->d_scratch) + 12;
+  CK(cudaMemsetAsync(mx, 0xFF, sizeof(int), c.s));
+  k_max_s32<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(color, n, mx);
+  int hmx = -1;
+  CK(cudaMemcpyAsync(&hmx, mx, sizeof hmx, cudaMemcpyDeviceToHost, c.s));
+  CKS(copy_out(color_out, color, (size_t)n * sizeof(int32_t), c.s));
+  CK(cudaStreamSynchronize(c.s));
+  if (ncolors_out) *ncolors_out = hmx + 1;
+  if (st) st->num_colors = hmx + 1;
+  return ATOS_OK;
+}

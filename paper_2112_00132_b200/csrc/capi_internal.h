@@ -1,0 +1,56 @@
+// capi_internal.h — host-side structures shared by capi.cu and dist.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/atos.h"
+#include "device.cuh"
+
+struct Workspace {
+  uint64_t* ring = nullptr;
+  uint64_t cap = 0;
+  uint64_t dirty = 0;  // ring slots that may hold non-zero tags
+  atos::QueueCtl* ctl = nullptr;
+  atos::QueueCtl* h_ctl = nullptr;  // pinned mirror
+  uint32_t* u32a = nullptr;         // BFS dist / GC pend
+  size_t u32a_n = 0;
+  float* f32a = nullptr;  // PR rank / GC colour
+  size_t f32a_n = 0;
+  float* f32b = nullptr;  // PR residue
+  size_t f32b_n = 0;
+  uint32_t* front[2] = {nullptr, nullptr};
+  size_t front_n[2] = {0, 0};
+  unsigned long long* fcount = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+struct DistState;  // dist.cu
+
+struct atos_graph_s {
+  int64_t n = 0;  // local vertex count (== global n when not partitioned)
+  int64_t m = 0;
+  int64_t max_degree = 0;
+  int64_t* d_off = nullptr;
+  int32_t* d_col = nullptr;
+  void* d_scratch = nullptr;
+  bool owned = false;
+  bool symmetric = false;
+  int device = 0;
+  int sms = 0;
+  Workspace ws;
+  // multi-GPU partition (dist.cu)
+  atos_comm comm = nullptr;
+  int64_t global_n = 0, v_begin = 0, v_end = 0;
+  DistState* dist = nullptr;
+};
+
+atos_status atos_set_error(atos_status s, const char* fmt, ...);
+atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* col, int64_t n, int64_t m,
+                              uint32_t flags);
+atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, uint64_t default_cap, bool need_ring,
+                       cudaStream_t s);
+atos_status dist_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t* depth_out, atos_stats* st);
+atos_status dist_pagerank(atos_graph g, float alpha, float eps, const atos_config* cfg, float* rank_out,
+                          atos_stats* st);
+void dist_free(atos_graph g);

@@ -1,0 +1,297 @@
+// device.cuh — memory-model helpers, the shared task queue and the termination
+// detector of the Atos hot path, sm_100a.
+//
+// The queue is ONE ring shared by every worker of the GPU (PAPER.md P:97,
+// "a single queue balances load more quickly"; Listing 2).
+//
+//  * ring: uint64 slots, capacity a power of two.  A slot word is
+//    (tag << 32) | item.  For queue position p (lap L = p >> log2cap) the slot
+//    is "empty for lap L" when tag == 2L and "full for lap L" when
+//    tag == 2L+1.  All tags start at 0 (empty for lap 0).  A consumer that has
+//    read position p writes tag 2L+2 (empty for lap L+1).  This bounded-MPMC
+//    discipline makes wrap-around safe without assuming anything about how
+//    fast other workers are.
+//  * head (next position to pop), tail (next position to push) and processed
+//    (items fully processed, including their pushes) are 64-bit counters, each
+//    on its own 128-byte line.
+//  * push (a3): warp-aggregated — __ballot_sync/__popc, ONE atomicAdd(tail)
+//    per warp, then each lane publishes its slot with st.release.gpu.
+//  * pop (a4): the worker leader reads head/tail and claims
+//    n = min(FETCH, tail - head) positions with one 64-bit CAS on head; all
+//    claimed positions have a reserved producer, so the consumer only waits
+//    for an in-flight store (no overshoot, no waiting on future pushes).
+//  * termination (a7): a worker adds its batch size to `processed` (release)
+//    only after all pushes of that batch are reserved.  An idle worker reads
+//    processed (acquire) THEN tail; processed == tail means every pushed item
+//    has been fully processed and nobody holds work: quiescence, exit.
+//  * overflow: a producer whose slot still holds an unconsumed item of the
+//    previous lap while head <= p - cap (more than cap live items) raises
+//    ATOS_ERR_QUEUE_OVERFLOW and aborts the run.
+//  * watchdog: idle/spin loops compare %globaltimer with a deadline and abort
+//    with ATOS_ERR_TIMEOUT.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace atos {
+
+constexpr unsigned FULL_MASK = 0xffffffffu;
+constexpr uint32_t GC_CHECK_BIT = 0x80000000u;  // colouring CHECK(v) tag (R10)
+
+enum : uint32_t { ABORT_NONE = 0, ABORT_OVERFLOW = 1, ABORT_TIMEOUT = 2 };
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t ld_relaxed_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_relaxed_f32(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_s32(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void atom_add_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// streaming read-only loads of immutable CSR arrays (no L1 allocation)
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_nc_s64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------- queue state
+struct alignas(128) Line64 {
+  uint64_t v;
+  uint64_t pad[15];
+};
+
+// Device-resident control block (one per run).
+struct QueueCtl {
+  Line64 head;
+  Line64 tail;
+  Line64 processed;
+  Line64 abort;         // ABORT_* code (u32 in .v)
+  Line64 high_water;    // max observed tail - head
+  Line64 stats[4];      // popped, pushed, edges, spare
+  Line64 aux[4];        // app-specific counters (e.g. PR check cursor, colours)
+};
+
+// Kernel-side view of the queue (passed by value).
+struct Queue {
+  uint64_t* ring;
+  uint64_t mask;      // cap - 1
+  uint32_t log2cap;
+  QueueCtl* ctl;
+  uint64_t deadline;    // %globaltimer deadline (ns); 0 = none (armed by q_arm)
+  uint64_t timeout_ns;  // 0 = no watchdog
+  uint64_t head_floor;  // discrete rounds: every position < head_floor is claimed
+};
+
+__device__ __forceinline__ bool q_aborted(const Queue& q) {
+  return ld_relaxed_u64(&q.ctl->abort.v) != 0;
+}
+__device__ __forceinline__ void q_raise(const Queue& q, uint32_t code) {
+  atomicCAS(reinterpret_cast<unsigned long long*>(&q.ctl->abort.v), 0ull, (unsigned long long)code);
+}
+__device__ __forceinline__ bool q_timed_out(const Queue& q) {
+  if (q.deadline == 0) return false;
+  if (globaltimer_ns() > q.deadline) { q_raise(q, ABORT_TIMEOUT); return true; }
+  return false;
+}
+// Arm the watchdog at kernel entry (deadline = now + timeout).
+__device__ __forceinline__ void q_arm(Queue& q) {
+  q.deadline = q.timeout_ns ? globaltimer_ns() + q.timeout_ns : 0;
+}
+
+// Publish `item` at queue position p (a3).  Waits only in the wrap-around case
+// for the previous lap's consumer; detects overflow.  Returns false on abort.
+__device__ __forceinline__ bool q_store_slot(const Queue& q, uint64_t p, uint32_t item) {
+  uint64_t* slot = q.ring + (p & q.mask);
+  const uint32_t lap = (uint32_t)(p >> q.log2cap);
+  if (lap > 0) {
+    // wait for "empty for lap" (tag 2*lap); previous lap's item must be consumed
+    unsigned ns = 32;
+    for (;;) {
+      uint32_t tag = (uint32_t)(ld_relaxed_u64(slot) >> 32);
+      if (tag == 2u * lap) break;
+      uint64_t h = ld_relaxed_u64(&q.ctl->head.v);
+      if (h < q.head_floor) h = q.head_floor;
+      if (h + q.mask + 1 <= p) {  // more than cap live (unclaimed) items
+        q_raise(q, ABORT_OVERFLOW);
+        return false;
+      }
+      if (q_aborted(q) || q_timed_out(q)) return false;
+      __nanosleep(ns);
+      ns = ns < 1024 ? ns * 2 : ns;
+    }
+  }
+  st_release_u64(slot, ((uint64_t)(2u * lap + 1u) << 32) | item);
+  return true;
+}
+
+// Read the item at position p (claimed by this worker) and mark the slot
+// empty for the next lap.  Returns false only on abort/timeout.
+__device__ __forceinline__ bool q_load_slot(const Queue& q, uint64_t p, uint32_t& item) {
+  uint64_t* slot = q.ring + (p & q.mask);
+  const uint32_t lap = (uint32_t)(p >> q.log2cap);
+  const uint32_t want = 2u * lap + 1u;
+  uint64_t w = ld_acquire_u64(slot);
+  if ((uint32_t)(w >> 32) != want) {
+    unsigned ns = 16;
+    for (;;) {
+      __nanosleep(ns);
+      w = ld_acquire_u64(slot);
+      if ((uint32_t)(w >> 32) == want) break;
+      if (q_aborted(q) || q_timed_out(q)) return false;
+      ns = ns < 256 ? ns * 2 : ns;
+    }
+  }
+  item = (uint32_t)w;
+  st_relaxed_u64(slot, (uint64_t)(2u * lap + 2u) << 32);
+  return true;
+}
+
+// Warp-collective push (every lane of the warp must call; `pred` per lane).
+// One atomicAdd on tail per warp.  Returns the number of items pushed.
+__device__ __forceinline__ uint32_t q_warp_push(const Queue& q, bool pred, uint32_t item) {
+  const unsigned mask = __ballot_sync(FULL_MASK, pred);
+  if (mask == 0) return 0;
+  const unsigned lane = lane_id();
+  const int leader = __ffs(mask) - 1;
+  const uint32_t cnt = __popc(mask);
+  unsigned long long base = 0;
+  if ((int)lane == leader) base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)cnt);
+  base = __shfl_sync(FULL_MASK, base, leader);
+  if (pred) q_store_slot(q, base + __popc(mask & lanemask_lt()), item);
+  return cnt;
+}
+
+// Push from a subset of converged lanes (thread workers with divergent loops):
+// aggregates over __activemask().
+__device__ __forceinline__ uint32_t q_active_push(const Queue& q, bool pred, uint32_t item) {
+  const unsigned act = __activemask();
+  const unsigned mask = __ballot_sync(act, pred);
+  if (mask == 0) return 0;
+  const unsigned lane = lane_id();
+  const int leader = __ffs(mask) - 1;
+  const uint32_t cnt = __popc(mask);
+  unsigned long long base = 0;
+  if ((int)lane == leader) base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)cnt);
+  base = __shfl_sync(act, base, leader);
+  if (pred) q_store_slot(q, base + __popc(mask & lanemask_lt()), item);
+  return cnt;
+}
+
+// Single-thread pop (a4): claim up to `want` positions.  Returns the count
+// claimed (0 if the queue is empty right now) and the first position.
+__device__ __forceinline__ uint32_t q_try_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& qlen) {
+  uint64_t h = ld_relaxed_u64(&q.ctl->head.v);
+  uint64_t t = ld_relaxed_u64(&q.ctl->tail.v);
+  for (int it = 0; it < 64; ++it) {
+    if (h >= t) {
+      t = ld_relaxed_u64(&q.ctl->tail.v);
+      if (h >= t) return 0;
+    }
+    const uint64_t avail = t - h;
+    const uint32_t n = avail < want ? (uint32_t)avail : want;
+    const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(&q.ctl->head.v),
+                                             (unsigned long long)h, (unsigned long long)(h + n));
+    if (old == h) {
+      first = h;
+      qlen = avail;
+      return n;
+    }
+    h = old;
+  }
+  return 0;
+}
+
+// Leader-side pop with the idle path (the paper's f2 hook): backoff,
+// termination poll (a7) and watchdog.  Returns n > 0 with `first`, or 0 when
+// the run is over (quiescent or aborted).
+__device__ __forceinline__ uint32_t q_pop_or_quit(const Queue& q, uint32_t want, uint64_t& first, uint64_t& hw) {
+  unsigned ns = 0;
+  if (q_aborted(q) || q_timed_out(q)) return 0;
+  for (;;) {
+    uint64_t qlen = 0;
+    uint32_t n = q_try_pop(q, want, first, qlen);
+    if (n) {
+      if (qlen > hw) hw = qlen;
+      return n;
+    }
+    // f2: failed pop.  Quiescence: processed (acquire) read BEFORE tail.
+    const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
+    const uint64_t t = ld_relaxed_u64(&q.ctl->tail.v);
+    if (p == t) return 0;
+    if (q_aborted(q) || q_timed_out(q)) return 0;
+    if (ns) __nanosleep(ns);
+    ns = ns == 0 ? 32 : (ns < 512 ? ns * 2 : ns);
+  }
+}
+
+// Mark `n` claimed items as fully processed (after all their pushes).
+__device__ __forceinline__ void q_done(const Queue& q, uint32_t n) {
+  atom_add_release_u64(&q.ctl->processed.v, (uint64_t)n);
+}
+
+// Per-worker statistics accumulated in registers and flushed once at exit.
+struct LocalStats {
+  uint64_t popped = 0, pushed = 0, edges = 0, hw = 0;
+  __device__ __forceinline__ void flush(const Queue& q) {
+    if (popped) atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->stats[0].v), (unsigned long long)popped);
+    if (pushed) atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->stats[1].v), (unsigned long long)pushed);
+    if (edges) atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->stats[2].v), (unsigned long long)edges);
+    if (hw) atomicMax(reinterpret_cast<unsigned long long*>(&q.ctl->high_water.v), (unsigned long long)hw);
+  }
+};
+
+}  // namespace atos

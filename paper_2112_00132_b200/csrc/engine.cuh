@@ -1,0 +1,377 @@
+// engine.cuh — worker expansion and the edge-map
+// applications BFS (a6-BFS) and push PageRank (a6-PR) for sm_100a.
+//
+// A worker takes a batch of popped vertices and, for each, visits its CSR
+// out-edges, applies the app's relaxed update to the neighbour and pushes the
+// neighbour if it was activated (Listing 2).  Worker
+// sizes:
+//   THREAD  one lane per vertex, serial neighbour walk (SIMT cursor loop);
+//   WARP    the paper's persist-32: the warp walks one vertex's list
+//           at a time, lanes striding with 16-byte int4 loads of col[];
+//   CTA     the paper's persist-CTA: block exclusive scan of the
+//           batch's degrees, then load-balancing search over the
+//           flattened edge range — thread e finds its vertex by binary search
+//           of the shared-memory prefix.  Each thread carries UNROLL edges per
+//           step so UNROLL col loads and UNROLL atomics are in flight.
+// Item sources and push sinks are templates so the same expansion serves the
+// persistent and discrete schedulers (ring queue) and the BSP variant
+// (frontier arrays).
+#pragma once
+#include "device.cuh"
+
+namespace atos {
+
+struct GraphView {
+  const int64_t* off;
+  const int32_t* col;
+  int64_t n;
+};
+
+// ------------------------------------------------------------------ apps ---
+
+// Speculative BFS relax (Alg. 2): d = current dist[v] (R3);
+// per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
+// (strict, R2).
+struct BfsApp {
+  uint32_t* dist;
+  int filter;
+  using Payload = uint32_t;
+  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
+                                        Payload& p) const {
+    e0 = ld_nc_s64(g.off + v);
+    e1 = ld_nc_s64(g.off + v + 1);
+    p = ld_relaxed_u32(dist + v) + 1u;
+    return e1 > e0;
+  }
+  __device__ __forceinline__ bool edge(Payload nd, uint32_t w) const {
+    if (filter && nd >= ld_relaxed_u32(dist + w)) return false;
+    return nd < atomicMin(dist + w, nd);
+  }
+};
+
+// Push PageRank (Alg. 4 body; dangling R5; activation R6):
+// r = atomicExch(res[v], 0); rank[v] += r; c = alpha r / deg(v);
+// per edge: old = atomicAdd(res[w], c); push w iff old <= eps < old + c.
+struct PrApp {
+  float* rank;
+  float* res;
+  float alpha, eps;
+  using Payload = float;
+  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
+                                        Payload& p) const {
+    e0 = ld_nc_s64(g.off + v);
+    e1 = ld_nc_s64(g.off + v + 1);
+    const float r = atomicExch(res + v, 0.0f);
+    if (r == 0.0f) return false;
+    atomicAdd(rank + v, r);
+    if (e1 == e0) return false;
+    p = __fdiv_rn(__fmul_rn(alpha, r), (float)(e1 - e0));
+    return true;
+  }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
+    const float old = atomicAdd(res + w, c);
+    return old <= eps && __fadd_rn(old, c) > eps;
+  }
+};
+
+// BSP PageRank push kernel body (Alg. 3 lines 11-16): same push
+// but the frontier is rebuilt by the filter kernel, so nothing is appended.
+struct PrBspApp {
+  PrApp base;
+  using Payload = float;
+  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
+                                        Payload& p) const {
+    return base.begin(v, g, e0, e1, p);
+  }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
+    atomicAdd(base.res + w, c);
+    return false;
+  }
+};
+
+// ------------------------------------------------------- sources / sinks ---
+
+struct RingSrc {
+  Queue q;
+  uint64_t first;
+  __device__ __forceinline__ bool get(uint32_t i, uint32_t& item) const { return q_load_slot(q, first + i, item); }
+};
+struct ArraySrc {
+  const uint32_t* a;
+  __device__ __forceinline__ bool get(uint32_t i, uint32_t& item) const {
+    item = a[i];
+    return true;
+  }
+};
+
+struct RingSink {
+  Queue q;
+  __device__ __forceinline__ uint32_t warp_push(bool pred, uint32_t item) const { return q_warp_push(q, pred, item); }
+  __device__ __forceinline__ uint32_t active_push(bool pred, uint32_t item) const { return q_active_push(q, pred, item); }
+};
+// BSP out-frontier: warp-aggregated append to out[count++].
+struct ArraySink {
+  uint32_t* out;
+  unsigned long long* count;
+  __device__ __forceinline__ uint32_t warp_push(bool pred, uint32_t item) const {
+    const unsigned mask = __ballot_sync(FULL_MASK, pred);
+    if (!mask) return 0;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(count, (unsigned long long)__popc(mask));
+    base = __shfl_sync(FULL_MASK, base, leader);
+    if (pred) out[base + __popc(mask & lanemask_lt())] = item;
+    return __popc(mask);
+  }
+  __device__ __forceinline__ uint32_t active_push(bool pred, uint32_t item) const {
+    const unsigned act = __activemask();
+    const unsigned mask = __ballot_sync(act, pred);
+    if (!mask) return 0;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(count, (unsigned long long)__popc(mask));
+    base = __shfl_sync(act, base, leader);
+    if (pred) out[base + __popc(mask & lanemask_lt())] = item;
+    return __popc(mask);
+  }
+};
+
+// ------------------------------------------------------ CTA worker (LBS) ---
+
+template <class Payload>
+struct CtaSmem {
+  int64_t* e0;    // [F]   first edge of batch item i
+  int64_t* pre;   // [F+1] exclusive prefix of degrees (LBS offsets)
+  Payload* pay;   // [F]
+  int64_t* wsum;  // [32]  scan scratch
+};
+
+template <class Payload>
+__host__ __device__ constexpr size_t cta_smem_bytes(int F) {
+  return (size_t)F * 8 + ((size_t)F + 1) * 8 + (size_t)F * sizeof(Payload) + 32 * 8 + 64;
+}
+
+template <class Payload>
+__device__ __forceinline__ CtaSmem<Payload> cta_smem_carve(unsigned char* base, int F) {
+  CtaSmem<Payload> s;
+  s.e0 = reinterpret_cast<int64_t*>(base);
+  s.pre = s.e0 + F;
+  s.wsum = s.pre + F + 1;
+  s.pay = reinterpret_cast<Payload*>(s.wsum + 32);
+  return s;
+}
+
+// In-place exclusive scan of a[0..n) (n <= F) into a[0..n], a[n] = total.
+// Each thread scans a contiguous segment; warp shuffles; one smem pass.
+__device__ __forceinline__ void block_exclusive_scan(int64_t* a, int n, int64_t* wsum) {
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int per = (n + T - 1) / T;
+  const int b = min(n, tid * per), e = min(n, b + per);
+  int64_t s = 0;
+  for (int i = b; i < e; ++i) s += a[i];
+  // inclusive warp scan of s
+  int64_t x = s;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int64_t y = __shfl_up_sync(FULL_MASK, x, d);
+    if ((int)lane_id() >= d) x += y;
+  }
+  const int wid = tid >> 5, nw = (T + 31) >> 5;
+  if ((int)lane_id() == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t v = (int)lane_id() < nw ? wsum[lane_id()] : 0;
+    int64_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int64_t y = __shfl_up_sync(FULL_MASK, inc, d);
+      if ((int)lane_id() >= d) inc += y;
+    }
+    if ((int)lane_id() < nw) wsum[lane_id()] = inc - v;  // exclusive warp offsets
+  }
+  __syncthreads();
+  int64_t run = wsum[wid] + x - s;  // exclusive prefix of this thread's segment
+  for (int i = b; i < e; ++i) {
+    int64_t d = a[i];
+    a[i] = run;
+    run += d;
+  }
+  if (tid == T - 1) a[n] = run;  // last thread's segment ends at n
+  __syncthreads();
+}
+
+// largest i in [0, n) with pre[i] <= e  (pre is non-decreasing, pre[0] = 0)
+__device__ __forceinline__ int lbs_find(const int64_t* pre, int n, int64_t e) {
+  int lo = 0, hi = n;  // invariant: pre[lo] <= e < pre[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (pre[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+constexpr int LBS_UNROLL = 4;
+
+// Process batch items [0, n) with the whole CTA.  Every thread must call.
+template <class App, class Src, class Sink>
+__device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, const Src& src, const Sink& sink,
+                                          uint32_t n, CtaSmem<typename App::Payload>& sm, LocalStats& st) {
+  using Payload = typename App::Payload;
+  const int T = blockDim.x, tid = threadIdx.x;
+  for (int i = tid; i < (int)n; i += T) {
+    uint32_t item = 0;
+    int64_t e0 = 0, e1 = 0;
+    Payload p{};
+    bool ok = src.get(i, item) && app.begin(item, g, e0, e1, p);
+    sm.e0[i] = e0;
+    sm.pre[i] = ok ? e1 - e0 : 0;
+    sm.pay[i] = p;
+  }
+  __syncthreads();
+  block_exclusive_scan(sm.pre, (int)n, sm.wsum);
+  const int64_t total = sm.pre[n];
+  const int wid = tid >> 5, lane = lane_id();
+  const int64_t stride = (int64_t)T * LBS_UNROLL;
+  uint32_t pushed = 0;
+  for (int64_t eb = (int64_t)wid * 32 * LBS_UNROLL; eb < total; eb += stride) {
+    int32_t w[LBS_UNROLL];
+    int idx[LBS_UNROLL];
+#pragma unroll
+    for (int k = 0; k < LBS_UNROLL; ++k) {
+      const int64_t e = eb + lane + 32 * k;
+      idx[k] = -1;
+      if (e < total) {
+        idx[k] = lbs_find(sm.pre, (int)n, e);
+        w[k] = ld_stream_s32(g.col + sm.e0[idx[k]] + (e - sm.pre[idx[k]]));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < LBS_UNROLL; ++k) {
+      const bool act = idx[k] >= 0 && app.edge(sm.pay[idx[k]], (uint32_t)w[k]);
+      pushed += sink.warp_push(act, (uint32_t)w[k]);
+    }
+  }
+  if (lane == 0) st.pushed += pushed;
+  if (tid == 0) st.edges += total;
+  __syncthreads();
+}
+
+// ---------------------------------------------------------- warp worker ---
+
+// Visit edges [e0, e1) of one vertex with the whole warp: scalar head up to a
+// 16-byte boundary, int4 body (4 edges per lane per step), scalar tail.
+template <class App, class Sink>
+__device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g, const Sink& sink, int64_t e0,
+                                              int64_t e1, typename App::Payload p) {
+  const int lane = lane_id();
+  uint32_t pushed = 0;
+  int64_t a0 = (e0 + 3) & ~int64_t(3);
+  if (a0 > e1) a0 = e1;
+  // head (< 4 edges) + tail share one scalar step each
+  {
+    const int64_t e = e0 + lane;
+    const bool v = e < a0;
+    int32_t w = v ? ld_stream_s32(g.col + e) : 0;
+    bool act = v && app.edge(p, (uint32_t)w);
+    pushed += sink.warp_push(act, (uint32_t)w);
+  }
+  const int64_t a1 = a0 + ((e1 - a0) & ~int64_t(3));
+  const int4* body = reinterpret_cast<const int4*>(g.col + a0);
+  const int64_t nv = (a1 - a0) >> 2;
+  for (int64_t vb = 0; vb < nv; vb += 32) {
+    const int64_t vi = vb + lane;
+    const bool v = vi < nv;
+    int4 w4 = v ? ld_stream_v4(body + vi) : make_int4(0, 0, 0, 0);
+    bool a = v && app.edge(p, (uint32_t)w4.x);
+    bool b = v && app.edge(p, (uint32_t)w4.y);
+    bool c = v && app.edge(p, (uint32_t)w4.z);
+    bool d = v && app.edge(p, (uint32_t)w4.w);
+    pushed += sink.warp_push(a, (uint32_t)w4.x);
+    pushed += sink.warp_push(b, (uint32_t)w4.y);
+    pushed += sink.warp_push(c, (uint32_t)w4.z);
+    pushed += sink.warp_push(d, (uint32_t)w4.w);
+  }
+  {
+    const int64_t e = a1 + lane;
+    const bool v = e < e1;
+    int32_t w = v ? ld_stream_s32(g.col + e) : 0;
+    bool act = v && app.edge(p, (uint32_t)w);
+    pushed += sink.warp_push(act, (uint32_t)w);
+  }
+  return pushed;
+}
+
+// Process batch items [0, n) with one warp (persist-32: no in-worker LB).
+template <class App, class Src, class Sink>
+__device__ __forceinline__ void warp_batch(const App& app, const GraphView& g, const Src& src, const Sink& sink,
+                                           uint32_t n, LocalStats& st) {
+  using Payload = typename App::Payload;
+  const int lane = lane_id();
+  uint32_t pushed = 0;
+  uint64_t edges = 0;
+  for (uint32_t c = 0; c < n; c += 32) {
+    const uint32_t k = min(32u, n - c);
+    int64_t e0 = 0, e1 = 0;
+    Payload p{};
+    bool ok = false;
+    if ((uint32_t)lane < k) {
+      uint32_t item;
+      ok = src.get(c + lane, item) && app.begin(item, g, e0, e1, p);
+    }
+    unsigned todo = __ballot_sync(FULL_MASK, ok);
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t je0 = __shfl_sync(FULL_MASK, e0, j);
+      const int64_t je1 = __shfl_sync(FULL_MASK, e1, j);
+      const Payload jp = __shfl_sync(FULL_MASK, p, j);
+      pushed += warp_walk(app, g, sink, je0, je1, jp);
+      edges += je1 - je0;
+    }
+  }
+  if (lane == 0) {
+    st.pushed += pushed;
+    st.edges += edges;
+  }
+}
+
+// -------------------------------------------------------- thread worker ---
+
+// Each lane owns items lane, lane+32, ... of the warp's batch [0, n) and walks
+// their edges serially; pushes aggregate over the lanes active in a step.
+template <class App, class Src, class Sink>
+__device__ __forceinline__ void thread_batch(const App& app, const GraphView& g, const Src& src, const Sink& sink,
+                                             uint32_t n, LocalStats& st) {
+  using Payload = typename App::Payload;
+  const uint32_t lane = lane_id();
+  uint32_t next = lane;
+  int64_t e = 0, e1 = 0;
+  Payload p{};
+  uint32_t pushed = 0;
+  uint64_t edges = 0;
+  auto refill = [&]() {
+    while (e >= e1 && next < n) {
+      uint32_t item;
+      int64_t b = 0, c = 0;
+      bool ok = src.get(next, item) && app.begin(item, g, b, c, p);
+      next += 32;
+      if (ok) { e = b; e1 = c; edges += c - b; }
+    }
+  };
+  refill();
+  while (__any_sync(FULL_MASK, e < e1)) {
+    bool act = false;
+    int32_t w = 0;
+    if (e < e1) {
+      w = ld_stream_s32(g.col + e);
+      ++e;
+      act = app.edge(p, (uint32_t)w);
+    }
+    pushed += sink.warp_push(act, (uint32_t)w);
+    refill();
+  }
+  st.edges += edges;
+  if (lane == 0) st.pushed += pushed;
+}
+
+}  // namespace atos

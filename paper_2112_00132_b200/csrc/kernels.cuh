@@ -1,0 +1,299 @@
+// kernels.cuh — the three kernel strategies (PAPER.md
+// P:264) over any worker policy:
+//   k_persistent  one launch; workers loop pop -> process -> push until the
+//                 termination detector fires (Listing 2).
+//   k_discrete    one launch per round over the queue snapshot [h, t) with
+//                 static slot assignment (no pop atomics); pushes land beyond t.
+//   k_bsp         one launch per BSP step over an explicit frontier array
+//                 (Alg. 1/3/5), appending to an out-frontier.
+#pragma once
+#include "gc.cuh"
+
+namespace atos {
+
+enum WorkerKind : int { W_THREAD = 0, W_WARP = 1, W_CTA = 2 };
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------- policies
+template <class App>
+struct EdgeMapPolicy {
+  using Payload = typename App::Payload;
+  static __host__ __device__ size_t smem_bytes(int F) { return cta_smem_bytes<Payload>(F); }
+  template <class Src, class Sink>
+  static __device__ __forceinline__ void cta(const App& app, const GraphView& g, const Src& src, const Sink& sink,
+                                             uint32_t n, unsigned char* smem, int F, LocalStats& st) {
+    CtaSmem<Payload> sm = cta_smem_carve<Payload>(smem, F);
+    cta_batch(app, g, src, sink, n, sm, st);
+  }
+  template <class Src, class Sink>
+  static __device__ __forceinline__ void warp(const App& app, const GraphView& g, const Src& src, const Sink& sink,
+                                              uint32_t n, LocalStats& st) {
+    warp_batch(app, g, src, sink, n, st);
+  }
+  template <class Src, class Sink>
+  static __device__ __forceinline__ void thread(const App& app, const GraphView& g, const Src& src,
+                                                const Sink& sink, uint32_t n, LocalStats& st) {
+    thread_batch(app, g, src, sink, n, st);
+  }
+};
+
+template <int MODE>
+struct GcPolicy {
+  static __host__ __device__ size_t smem_bytes(int F) { return gc_cta_smem_bytes(F); }
+  template <class Src, class Sink>
+  static __device__ __forceinline__ void cta(const GcApp& app, const GraphView& g, const Src& src, const Sink& sink,
+                                             uint32_t n, unsigned char* smem, int F, LocalStats& st) {
+    GcCtaSmem sm = gc_smem_carve(smem, F);
+    gc_cta_batch<MODE>(app, g, src, sink, n, sm, st);
+  }
+  template <class Src, class Sink>
+  static __device__ __forceinline__ void warp(const GcApp& app, const GraphView& g, const Src& src, const Sink& sink,
+                                              uint32_t n, LocalStats& st) {
+    uint64_t edges = 0;
+    uint32_t pushed = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      uint32_t t = 0;
+      bool ok = true;
+      if (lane_id() == 0) ok = src.get(j, t);
+      ok = __shfl_sync(FULL_MASK, ok, 0);
+      t = __shfl_sync(FULL_MASK, t, 0);
+      if (!ok) continue;
+      if (MODE == GC_BSP_DETECT) t |= GC_CHECK_BIT;
+      pushed += gc_warp_task<MODE>(app, g, sink, t, edges);
+    }
+    if (lane_id() == 0) {
+      st.pushed += pushed;
+      st.edges += edges;
+    }
+  }
+  template <class Src, class Sink>
+  static __device__ __forceinline__ void thread(const GcApp& app, const GraphView& g, const Src& src,
+                                                const Sink& sink, uint32_t n, LocalStats& st) {
+    uint64_t edges = 0;
+    uint32_t pushed = 0;
+    for (uint32_t base = 0; base < n; base += 32) {
+      const uint32_t j = base + lane_id();
+      uint32_t t = 0;
+      bool ok = j < n && src.get(j, t);
+      if (MODE == GC_BSP_DETECT) t |= GC_CHECK_BIT;
+      pushed += gc_thread_task<MODE>(app, g, sink, ok, t, edges);
+    }
+    st.edges += edges;
+    if (lane_id() == 0) st.pushed += pushed;
+  }
+};
+
+// ------------------------------------------------------------ persistent
+template <class P, class App, int W>
+__global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Queue q0, int F) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Queue q = q0;
+  q_arm(q);
+  LocalStats st;
+  RingSink sink{q};
+  if (W == W_CTA) {
+    __shared__ uint64_t s_first;
+    __shared__ uint32_t s_n;
+    for (;;) {
+      if (threadIdx.x == 0) {
+        uint64_t first = 0;
+        uint32_t n = q_pop_or_quit(q, (uint32_t)F, first, st.hw);
+        s_first = first;
+        s_n = n;
+      }
+      __syncthreads();
+      const uint32_t n = s_n;
+      const uint64_t first = s_first;
+      if (n == 0) break;
+      RingSrc src{q, first};
+      P::cta(app, g, src, sink, n, smem, F, st);  // ends with __syncthreads
+      if (threadIdx.x == 0) {
+        st.popped += n;
+        q_done(q, n);
+      }
+    }
+  } else {
+    const uint32_t want = (W == W_WARP) ? (uint32_t)F : 32u * (uint32_t)F;
+    for (;;) {
+      uint64_t first = 0;
+      uint32_t n = 0;
+      if (lane_id() == 0) n = q_pop_or_quit(q, want, first, st.hw);
+      n = __shfl_sync(FULL_MASK, n, 0);
+      first = __shfl_sync(FULL_MASK, first, 0);
+      if (n == 0) break;
+      RingSrc src{q, first};
+      if (W == W_WARP) P::warp(app, g, src, sink, n, st);
+      else P::thread(app, g, src, sink, n, st);
+      __syncwarp();
+      if (lane_id() == 0) {
+        st.popped += n;
+        q_done(q, n);
+      }
+    }
+  }
+  st.flush(q);
+}
+
+// ------------------------------------------------------------ discrete
+// Round over queue positions [h, t); worker k owns [h + k*chunk, ...).
+template <class P, class App, int W>
+__global__ void __launch_bounds__(1024, 1) k_discrete(App app, GraphView g, Queue q0, uint64_t h, uint64_t t, int F) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Queue q = q0;
+  q_arm(q);
+  LocalStats st;
+  RingSink sink{q};
+  const uint64_t S = t - h;
+  if (W == W_CTA) {
+    for (uint64_t k = blockIdx.x; k * (uint64_t)F < S; k += gridDim.x) {
+      const uint64_t first = h + k * (uint64_t)F;
+      const uint32_t n = (uint32_t)umin64((uint64_t)F, t - first);
+      RingSrc src{q, first};
+      P::cta(app, g, src, sink, n, smem, F, st);
+      if (threadIdx.x == 0) st.popped += n;
+    }
+  } else {
+    const uint64_t chunk = (W == W_WARP) ? (uint64_t)F : 32ull * (uint64_t)F;
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t nw = (uint64_t)gridDim.x * wpb;
+    for (uint64_t k = blockIdx.x * wpb + (threadIdx.x >> 5); k * chunk < S; k += nw) {
+      const uint64_t first = h + k * chunk;
+      const uint32_t n = (uint32_t)umin64(chunk, t - first);
+      RingSrc src{q, first};
+      if (W == W_WARP) P::warp(app, g, src, sink, n, st);
+      else P::thread(app, g, src, sink, n, st);
+      if (lane_id() == 0) st.popped += n;
+    }
+  }
+  st.flush(q);
+}
+
+// ------------------------------------------------------------ BSP
+struct OffsetSrc {
+  const uint32_t* a;
+  __device__ __forceinline__ bool get(uint32_t i, uint32_t& item) const {
+    item = a[i];
+    return true;
+  }
+};
+struct IotaSrc {
+  uint32_t base;
+  __device__ __forceinline__ bool get(uint32_t i, uint32_t& item) const {
+    item = base + i;
+    return true;
+  }
+};
+struct NullSink {
+  __device__ __forceinline__ uint32_t warp_push(bool, uint32_t) const { return 0; }
+  __device__ __forceinline__ uint32_t active_push(bool, uint32_t) const { return 0; }
+};
+
+// in == nullptr: the frontier is all vertices [0, count).
+template <class P, class App, int W>
+__global__ void __launch_bounds__(1024, 1) k_bsp(App app, GraphView g, const uint32_t* in, uint64_t count,
+                                              uint32_t* out, unsigned long long* out_count, QueueCtl* ctl, int F) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  LocalStats st;
+  ArraySink sink{out, out_count};
+  const uint64_t chunk = (W == W_CTA) ? (uint64_t)F : (W == W_WARP ? (uint64_t)F : 32ull * (uint64_t)F);
+  uint64_t k, step;
+  if (W == W_CTA) { k = blockIdx.x; step = gridDim.x; }
+  else { k = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); step = (uint64_t)gridDim.x * (blockDim.x >> 5); }
+  for (; k * chunk < count; k += step) {
+    const uint64_t first = k * chunk;
+    const uint32_t n = (uint32_t)umin64(chunk, count - first);
+    if (in) {
+      OffsetSrc src{in + first};
+      if (W == W_CTA) P::cta(app, g, src, sink, n, smem, F, st);
+      else if (W == W_WARP) P::warp(app, g, src, sink, n, st);
+      else P::thread(app, g, src, sink, n, st);
+    } else {
+      IotaSrc src{(uint32_t)first};
+      if (W == W_CTA) P::cta(app, g, src, sink, n, smem, F, st);
+      else if (W == W_WARP) P::warp(app, g, src, sink, n, st);
+      else P::thread(app, g, src, sink, n, st);
+    }
+    if ((W == W_CTA && threadIdx.x == 0) || (W != W_CTA && lane_id() == 0)) st.popped += n;
+  }
+  if (ctl) {
+    Queue q{};
+    q.ctl = ctl;
+    st.hw = 0;
+    st.flush(q);
+  }
+}
+
+// ------------------------------------------------------------ small kernels
+template <class T>
+__global__ void k_fill(T* a, int64_t n, T v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = v;
+}
+
+// ring[p] = full(lap 0) | item(p) for p < n; item = p (| tag)
+__global__ void k_ring_prefill(uint64_t* ring, int64_t n, uint32_t tag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    ring[i] = (1ull << 32) | (uint64_t)((uint32_t)i | tag);
+}
+
+// Initialise the control block: head = 0, tail = processed-base, etc.
+__global__ void k_ctl_init(QueueCtl* ctl, uint64_t tail, uint64_t* ring, int64_t src_item) {
+  ctl->head.v = 0;
+  ctl->tail.v = tail;
+  ctl->processed.v = 0;
+  ctl->abort.v = 0;
+  ctl->high_water.v = tail;
+  for (int i = 0; i < 4; ++i) { ctl->stats[i].v = 0; ctl->aux[i].v = 0; }
+  if (src_item >= 0) ring[0] = (1ull << 32) | (uint64_t)(uint32_t)src_item;
+}
+
+// BFS init: dist[:] = MAX, dist[src] = 0 (R1)
+__global__ void k_bfs_init(uint32_t* dist, int64_t n, int64_t src) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dist[i] = (i == src) ? 0u : 0xFFFFFFFFu;
+}
+
+// PR residue seeding (reading R4 of Alg. 3 lines 5-7): the edge-map of an
+// app that pushes c = (1-a) a / deg(v) to every out-neighbour, no activation.
+struct PrInitApp {
+  float* res;
+  float c0;  // (1 - alpha) * alpha
+  using Payload = float;
+  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1, Payload& p) const {
+    e0 = ld_nc_s64(g.off + v);
+    e1 = ld_nc_s64(g.off + v + 1);
+    if (e1 == e0) return false;
+    p = __fdiv_rn(c0, (float)(e1 - e0));
+    return true;
+  }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
+    atomicAdd(res + w, c);
+    return false;
+  }
+};
+
+// BSP PageRank filter kernel (Alg. 3 lines 18-22): residue > eps -> frontier
+__global__ void k_pr_filter(const float* res, int64_t n, float eps, uint32_t* out, unsigned long long* count) {
+  ArraySink sink{out, count};
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = b + lane_id();
+    const bool a = v < n && res[v] > eps;
+    sink.warp_push(a, (uint32_t)v);
+  }
+}
+
+// max reduction helpers for stats
+__global__ void k_max_f32(const float* a, int64_t n, unsigned int* out_bits) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) m = fmaxf(m, a[i]);
+  for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL_MASK, m, d));
+  if (lane_id() == 0) atomicMax(out_bits, __float_as_uint(m));  // m >= 0 so bit order == value order
+}
+__global__ void k_max_s32(const int32_t* a, int64_t n, int* out) {
+  int m = -1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) m = max(m, a[i]);
+  for (int d = 16; d; d >>= 1) m = max(m, __shfl_xor_sync(FULL_MASK, m, d));
+  if (lane_id() == 0) atomicMax(out, m);
+}
+
+}  // namespace atos

@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs.
+
+Acceptance (BASELINE.json north_star):
+  BFS        bit-exact depths;
+  PageRank   ||rank - x*||_inf <= 1e-4 * max(x*) vs the fp64 Jacobi oracle, and
+             every residue <= eps (device-reported);
+  colouring  zero monochromatic edges (exhaustive scan), color[v] <= deg(v);
+             colour count reported beside the oracle's, not asserted equal.
+"""
+import itertools
+import os
+
+import numpy as np
+import pytest
+
+import graphgen as gg
+import oracle
+
+pytestmark = pytest.mark.gpu
+PR_TOL = 1e-4
+
+KERNELS = ["persistent", "discrete", "bsp"]
+WORKERS = ["thread", "warp", "cta"]
+FETCH = [1, 4, 32, 256]
+
+
+@pytest.fixture(scope="module")
+def atos():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2112_00132_b200 as a
+    a.lib()
+    return a
+
+
+_cache = {}
+
+
+def G(name):
+    """Seeded test graphs (host CSR, cached)."""
+    if name not in _cache:
+        f = {
+            "grid64": lambda: gg.grid(64, 64),
+            "rmat16": lambda: gg.rmat(16, 16, seed=1),
+            "rmat16s": lambda: gg.rmat(16, 16, seed=1, symmetrize=True),
+            "rmat12": lambda: gg.rmat(12, 16, seed=1),
+            "rmat12s": lambda: gg.rmat(12, 16, seed=1, symmetrize=True),
+            "road": lambda: gg.grid(120, 90, drop_prob=0.4, seed=5),
+            "path": lambda: gg.path(3000),
+            "star": lambda: gg.star(5000),
+            "K9": lambda: gg.complete(9),
+            "hub": lambda: gg.hub_graph(70000, extra=300),
+            "two": lambda: gg.from_edges(10, [(0, 1), (1, 2), (5, 6), (6, 7), (7, 5)], symmetrize=True),
+            "empty5": lambda: gg.empty(5),
+        }[name]
+        _cache[name] = f()
+    return _cache[name]
+
+
+_dev = {}
+
+
+def D(atos, name, symmetric=False):
+    key = (name, symmetric)
+    if key not in _dev:
+        _dev[key] = atos.Graph.from_csr(G(name), symmetric=symmetric)
+    return _dev[key]
+
+
+# ------------------------------------------------------------------ BFS ---
+
+@pytest.mark.parametrize("kernel,worker,fetch", list(itertools.product(KERNELS, WORKERS, FETCH)))
+@pytest.mark.parametrize("gname", ["grid64", "rmat16"])
+def test_bfs_matrix(atos, gname, kernel, worker, fetch):
+    g = G(gname)
+    d, st = atos.bfs(D(atos, gname), 0, kernel=kernel, worker=worker, fetch_size=fetch)
+    exp = oracle.bfs(g, 0)
+    assert np.array_equal(d, exp), f"{int(np.sum(d != exp))} mismatches"
+    reach = int(np.sum(exp != oracle.UNREACHED))
+    assert st["tasks_popped"] >= reach  # overwork >= 1
+
+
+def test_bfs_grid_manhattan(atos):
+    d, _ = atos.bfs(D(atos, "grid64"), 0)
+    i, j = np.divmod(np.arange(64 * 64), 64)
+    assert np.array_equal(d, (i + j).astype(np.uint32)) and d.max() == 126
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_bfs_small_rmat_seeds(atos, seed):
+    # SPEC S:556 acceptance 1: oracle equivalence, 20 seeds
+    g = gg.rmat(10, 8, seed=seed)
+    G_ = atos.Graph.from_csr(g)
+    for cfg in [dict(), dict(worker="warp", fetch_size=4), dict(worker="thread", fetch_size=1, kernel="discrete")]:
+        d, _ = atos.bfs(G_, seed % g.n, **cfg)
+        assert np.array_equal(d, oracle.bfs(g, seed % g.n)), cfg
+
+
+@pytest.mark.parametrize("gname,src", [("path", 0), ("path", 1500), ("star", 0), ("star", 17), ("K9", 4),
+                                       ("hub", 0), ("two", 0), ("two", 5), ("two", 9), ("empty5", 2), ("road", 0)])
+@pytest.mark.parametrize("worker", WORKERS)
+def test_bfs_special_graphs(atos, gname, src, worker):
+    g = G(gname)
+    d, _ = atos.bfs(D(atos, gname), src, worker=worker, fetch_size=32)
+    assert np.array_equal(d, oracle.bfs(g, src))
+
+
+def test_bfs_serial_order_identity(atos):
+    """One warp worker, FETCH 1, one CTA: FIFO order => Dijkstra order =>
+    every reachable vertex is popped exactly once (overwork 1.0)."""
+    for name in ["grid64", "rmat12", "road"]:
+        g = G(name)
+        d, st = atos.bfs(D(atos, name), 0, worker="warp", fetch_size=1, num_blocks=1, cta_threads=32)
+        exp = oracle.bfs(g, 0)
+        assert np.array_equal(d, exp)
+        assert st["tasks_popped"] == int(np.sum(exp != oracle.UNREACHED)), name
+
+
+def test_bfs_device_output_and_torch_borrow(atos):
+    import torch
+    g = G("rmat12")
+    off = torch.from_numpy(g.off).cuda()
+    col = torch.from_numpy(g.col).cuda()
+    Gt = atos.Graph(off, col)
+    d, _ = atos.bfs(Gt, 3, device=True)
+    assert d.is_cuda
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), oracle.bfs(g, 3))
+
+
+def test_bfs_queue_wraparound(atos):
+    g = G("grid64")
+    d, st = atos.bfs(D(atos, "grid64"), 0, queue_capacity=256, worker="warp", fetch_size=4)
+    assert np.array_equal(d, oracle.bfs(g, 0))
+    assert st["tasks_pushed"] > 256  # wrapped the ring
+
+
+def test_bfs_queue_overflow(atos):
+    with pytest.raises(atos.AtosError) as e:
+        atos.bfs(D(atos, "star"), 0, queue_capacity=32, num_blocks=1)
+    assert e.value.name == "QUEUE_OVERFLOW"
+    # the handle stays usable
+    d, _ = atos.bfs(D(atos, "star"), 0)
+    assert np.array_equal(d, oracle.bfs(G("star"), 0))
+
+
+def test_bfs_errors(atos):
+    with pytest.raises(atos.AtosError) as e:
+        atos.bfs(D(atos, "grid64"), 4096)
+    assert e.value.name == "INVALID_ARGUMENT"
+    with pytest.raises(atos.AtosError):
+        atos.bfs(D(atos, "grid64"), 0, cta_threads=48)
+    with pytest.raises(atos.AtosError):
+        atos.bfs(D(atos, "grid64"), 0, fetch_size=0)
+    E = atos.Graph(np.zeros(1, np.int64), np.zeros(0, np.int32))
+    d, _ = atos.bfs(E, 0)  # n == 0: OK, nothing written
+    assert d.size == 0
+    with pytest.raises(atos.AtosError) as e:
+        atos.Graph(np.array([0, 2, 1], np.int64), np.array([0, 1], np.int32), validate=True)
+    assert e.value.name == "INVALID_GRAPH"
+    with pytest.raises(atos.AtosError) as e:
+        atos.Graph(np.array([0, 1, 2], np.int64), np.array([0, 7], np.int32), validate=True)
+    assert e.value.name == "INVALID_GRAPH"
+
+
+def test_watchdog_timeout(atos):
+    with pytest.raises(atos.AtosError) as e:
+        atos.pagerank(D(atos, "rmat16"), 0.85, 1e-9, timeout_s=1e-6, worker="thread", fetch_size=1)
+    assert e.value.name == "TIMEOUT"
+    r, st = atos.pagerank(D(atos, "rmat12"), 0.85, 1e-6)  # library still healthy
+    assert st["max_residue"] <= 1e-6
+
+
+# ------------------------------------------------------------- PageRank ---
+
+_jac = {}
+
+
+def jacobi(name, alpha=0.85):
+    if (name, alpha) not in _jac:
+        _jac[(name, alpha)] = oracle.pagerank(G(name), alpha)[0]
+    return _jac[(name, alpha)]
+
+
+@pytest.mark.parametrize("kernel,worker,fetch", [(k, w, f) for k in KERNELS for w in WORKERS for f in (1, 32, 256)])
+def test_pagerank_matrix(atos, kernel, worker, fetch):
+    x = jacobi("rmat16")
+    r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=fetch)
+    err = np.max(np.abs(r.astype(np.float64) - x)) / x.max()
+    assert err <= PR_TOL, err
+    assert st["max_residue"] <= 1e-6
+    # one-sided bound 0 <= x* - rank <= eps x*/(1-a) (+ fp32 rounding)
+    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
+
+
+@pytest.mark.parametrize("gname", ["grid64", "star", "K9", "path", "two", "road", "hub"])
+def test_pagerank_special(atos, gname):
+    x = jacobi(gname)
+    for cfg in [dict(), dict(worker="warp", fetch_size=8, kernel="discrete")]:
+        r, st = atos.pagerank(D(atos, gname), 0.85, 1e-6, **cfg)
+        assert np.max(np.abs(r - x)) / x.max() <= PR_TOL
+        assert st["max_residue"] <= 1e-6
+
+
+def test_pagerank_closed_forms(atos):
+    a = 0.85
+    r, _ = atos.pagerank(atos.Graph.from_csr(gg.star(5)), a, 1e-7)
+    assert abs(r[0] - (1 + a * 5) / (1 + a)) < 1e-4 and np.allclose(r[1:], (1 + a / 5) / (1 + a), atol=1e-5)
+    r, _ = atos.pagerank(atos.Graph.from_csr(gg.directed_chain(6)), a, 1e-7)
+    assert np.allclose(r, 1 - a ** (np.arange(6) + 1), atol=1e-5)
+    r, _ = atos.pagerank(atos.Graph.from_csr(gg.complete(8)), a, 1e-7)
+    assert np.allclose(r, 1.0, atol=1e-5)
+
+
+def test_pagerank_errors(atos):
+    for al, ep in [(0.0, 1e-6), (1.0, 1e-6), (0.85, 0.0), (0.85, float("nan"))]:
+        with pytest.raises(atos.AtosError) as e:
+            atos.pagerank(D(atos, "K9"), al, ep)
+        assert e.value.name == "INVALID_ARGUMENT"
+    with pytest.raises(atos.AtosError) as e:
+        atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, queue_capacity=1024)
+    assert e.value.name == "QUEUE_OVERFLOW"
+
+
+# ------------------------------------------------------------ colouring ---
+
+@pytest.mark.parametrize("kernel,worker,fetch", [(k, w, f) for k in KERNELS for w in WORKERS for f in (1, 32, 256)])
+def test_color_matrix(atos, kernel, worker, fetch):
+    g = G("rmat16s")
+    c, k, st = atos.color(D(atos, "rmat16s", symmetric=True), kernel=kernel, worker=worker, fetch_size=fetch)
+    bad, kk = oracle.check_coloring(g, c)
+    assert bad == 0
+    assert kk == k
+    _, k_or = oracle.greedy_color(g)
+    print(f"colours gpu={k} oracle={k_or} tasks={st['tasks_popped']} overwork={st['tasks_popped'] / (2 * g.n):.2f}")
+
+
+@pytest.mark.parametrize("worker", WORKERS)
+def test_color_closed_forms(atos, worker):
+    for kn in [2, 5, 9, 33]:
+        c, k, _ = atos.color(atos.Graph.from_csr(gg.complete(kn), symmetric=True), worker=worker)
+        assert k == kn and sorted(c.tolist()) == list(range(kn))
+    c, k, _ = atos.color(atos.Graph.from_csr(gg.empty(7), symmetric=True), worker=worker)
+    assert k == 1 and np.all(c == 0)
+    for name in ["grid64", "road", "path", "star", "two"]:
+        g = G(name)
+        c, k, _ = atos.color(D(atos, name, symmetric=True), worker=worker)
+        assert oracle.check_coloring(g, c)[0] == 0
+        assert k <= int(g.degrees().max()) + 1
+
+
+def test_color_requires_symmetric(atos):
+    with pytest.raises(atos.AtosError) as e:
+        atos.color(D(atos, "rmat16"))
+    assert e.value.name == "INVALID_GRAPH"
