@@ -320,8 +320,8 @@ template <class P, class App, int W>
 static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q) {
   auto kern = k_persistent<P, App, W>;
   const int F = c.cfg.fetch_size, T = c.cfg.cta_threads;
-  const size_t smem = (W == W_CTA) ? P::smem_bytes(F) : 0;
-  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d needs %zu B smem", F, smem);
+  const size_t smem = worker_smem_bytes<P>(W, F, T);
+  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
   CKS(set_smem(kern, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
@@ -356,8 +356,8 @@ template <class P, class App, int W>
 static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0) {
   auto kern = k_discrete<P, App, W>;
   const int F = c.cfg.fetch_size, T = c.cfg.cta_threads;
-  const size_t smem = (W == W_CTA) ? P::smem_bytes(F) : 0;
-  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d needs %zu B smem", F, smem);
+  const size_t smem = worker_smem_bytes<P>(W, F, T);
+  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
   CKS(set_smem(kern, smem));
   const uint64_t chunk = (W == W_CTA) ? (uint64_t)F : (W == W_WARP ? (uint64_t)F : 32ull * (uint64_t)F);
   const uint64_t per_block = (W == W_CTA) ? 1 : (uint64_t)(T / 32);
@@ -401,7 +401,7 @@ static atos_status bsp_step_w(LaunchCtx& c, const App& app, const uint32_t* in, 
   auto kern = k_bsp<P, App, W>;
   const int T = c.cfg.cta_threads;
   const size_t smem = (W == W_CTA) ? P::smem_bytes(F) : 0;
-  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d needs %zu B smem", F, smem);
+  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
   CKS(set_smem(kern, smem));
   const uint64_t chunk = (W == W_CTA) ? (uint64_t)F : (W == W_WARP ? (uint64_t)F : 32ull * (uint64_t)F);
   const uint64_t per_block = (W == W_CTA) ? 1 : (uint64_t)(T / 32);

@@ -84,6 +84,31 @@ struct GcPolicy {
   }
 };
 
+// Stage claimed ring positions [first, first+n) into shared memory (warp-collective).
+__device__ __forceinline__ void stage_items(const Queue& q, uint64_t first, uint32_t n, uint32_t* stage) {
+  for (uint32_t i = lane_id(); i < n; i += 32) {
+    uint32_t it = 0xFFFFFFFFu;
+    if (!q_load_slot(q, first + i, it)) it = 0xFFFFFFFFu;
+    stage[i] = it;
+  }
+  __syncwarp();
+}
+struct StageSrc {
+  const uint32_t* a;
+  __device__ __forceinline__ bool get(uint32_t i, uint32_t& item) const {
+    item = a[i];
+    return item != 0xFFFFFFFFu;
+  }
+};
+
+// dynamic shared memory per block for a worker kind
+template <class P>
+__host__ __device__ inline size_t worker_smem_bytes(int W, int F, int T) {
+  if (W == W_CTA) return P::smem_bytes(F);
+  if (W == W_WARP) return (size_t)(T / 32) * (size_t)F * 4;
+  return (size_t)T * (size_t)F * 4;
+}
+
 // ------------------------------------------------------------ persistent
 template <class P, class App, int W>
 __global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Queue q0, int F) {
@@ -114,7 +139,12 @@ __global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Qu
       }
     }
   } else {
+    // Warp / thread workers stage their claimed items in shared memory right
+    // after the pop (eager read): a worker never holds a claimed-but-unread
+    // slot while it pushes, so a producer waiting on a wrapped slot (lap > 0)
+    // can never wait on itself.
     const uint32_t want = (W == W_WARP) ? (uint32_t)F : 32u * (uint32_t)F;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem) + (size_t)(threadIdx.x >> 5) * want;
     for (;;) {
       uint64_t first = 0;
       uint32_t n = 0;
@@ -122,7 +152,8 @@ __global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Qu
       n = __shfl_sync(FULL_MASK, n, 0);
       first = __shfl_sync(FULL_MASK, first, 0);
       if (n == 0) break;
-      RingSrc src{q, first};
+      stage_items(q, first, n, stage);
+      StageSrc src{stage};
       if (W == W_WARP) P::warp(app, g, src, sink, n, st);
       else P::thread(app, g, src, sink, n, st);
       __syncwarp();
@@ -157,12 +188,15 @@ __global__ void __launch_bounds__(1024, 1) k_discrete(App app, GraphView g, Queu
     const uint64_t chunk = (W == W_WARP) ? (uint64_t)F : 32ull * (uint64_t)F;
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nw = (uint64_t)gridDim.x * wpb;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem) + (size_t)(threadIdx.x >> 5) * chunk;
     for (uint64_t k = blockIdx.x * wpb + (threadIdx.x >> 5); k * chunk < S; k += nw) {
       const uint64_t first = h + k * chunk;
       const uint32_t n = (uint32_t)umin64(chunk, t - first);
-      RingSrc src{q, first};
+      stage_items(q, first, n, stage);
+      StageSrc src{stage};
       if (W == W_WARP) P::warp(app, g, src, sink, n, st);
       else P::thread(app, g, src, sink, n, st);
+      __syncwarp();
       if (lane_id() == 0) st.popped += n;
     }
   }

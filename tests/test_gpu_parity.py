@@ -37,6 +37,11 @@ def atos():
 _cache = {}
 
 
+def T(worker, fetch):
+    """cta_threads: thread workers stage 32*FETCH items per warp in shared memory."""
+    return 128 if worker == "thread" and fetch > 128 else 256
+
+
 def G(name):
     """Seeded test graphs (host CSR, cached)."""
     if name not in _cache:
@@ -74,7 +79,8 @@ def D(atos, name, symmetric=False):
 @pytest.mark.parametrize("gname", ["grid64", "rmat16"])
 def test_bfs_matrix(atos, gname, kernel, worker, fetch):
     g = G(gname)
-    d, st = atos.bfs(D(atos, gname), 0, kernel=kernel, worker=worker, fetch_size=fetch)
+    d, st = atos.bfs(D(atos, gname), 0, kernel=kernel, worker=worker, fetch_size=fetch,
+                     cta_threads=T(worker, fetch))
     exp = oracle.bfs(g, 0)
     assert np.array_equal(d, exp), f"{int(np.sum(d != exp))} mismatches"
     reach = int(np.sum(exp != oracle.UNREACHED))
@@ -185,7 +191,8 @@ def jacobi(name, alpha=0.85):
 @pytest.mark.parametrize("kernel,worker,fetch", [(k, w, f) for k in KERNELS for w in WORKERS for f in (1, 32, 256)])
 def test_pagerank_matrix(atos, kernel, worker, fetch):
     x = jacobi("rmat16")
-    r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=fetch)
+    r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=fetch,
+                          cta_threads=T(worker, fetch))
     err = np.max(np.abs(r.astype(np.float64) - x)) / x.max()
     assert err <= PR_TOL, err
     assert st["max_residue"] <= 1e-6
@@ -227,7 +234,8 @@ def test_pagerank_errors(atos):
 @pytest.mark.parametrize("kernel,worker,fetch", [(k, w, f) for k in KERNELS for w in WORKERS for f in (1, 32, 256)])
 def test_color_matrix(atos, kernel, worker, fetch):
     g = G("rmat16s")
-    c, k, st = atos.color(D(atos, "rmat16s", symmetric=True), kernel=kernel, worker=worker, fetch_size=fetch)
+    c, k, st = atos.color(D(atos, "rmat16s", symmetric=True), kernel=kernel, worker=worker, fetch_size=fetch,
+                           cta_threads=T(worker, fetch))
     bad, kk = oracle.check_coloring(g, c)
     assert bad == 0
     assert kk == k
