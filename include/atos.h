@@ -70,6 +70,7 @@ typedef struct {
   int32_t pr_activation;  /* 0: threshold crossing (R6, default); 1: Check_Size window */
   int32_t check_size;     /* Alg. 4 Check_Size; used when pr_activation == 1          */
   int32_t gc_literal;     /* 1: paper-literal Alg. 6 (both endpoints recolour) — ablation only */
+  int32_t pr_residue_fp64; /* 1: PageRank residues in fp64 (rank is always fp64-accumulated)   */
   int64_t queue_capacity; /* ring slots; 0 = auto (power of two >= 2n); rounded up to pow2     */
   double timeout_s;       /* device watchdog deadline in seconds; 0 = none                    */
   void* stream;           /* cudaStream_t to run on; NULL = legacy default stream             */
@@ -80,7 +81,7 @@ typedef struct {
   uint32_t struct_size;
   double ms;                /* device time of init + run (CUDA events on cfg->stream)     */
   double kernel_ms;         /* device time of the hot-path kernels alone (sum)            */
-  int64_t kernel_launches;  /* hot-path kernel launches (1 for persistent)                */
+  int64_t kernel_launches;  /* every kernel this call launched (init + hot path + reductions) */
   int64_t tasks_popped;     /* queue items processed (vertices / colour tasks)            */
   int64_t tasks_pushed;     /* items pushed after init                                    */
   int64_t edges_processed;  /* edge visits (BFS relax attempts, PR edge pushes, GC scans) */

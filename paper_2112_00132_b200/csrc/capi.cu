@@ -76,6 +76,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->pr_activation = 0;
   c->check_size = 32;
   c->gc_literal = 0;
+  c->pr_residue_fp64 = 0;
   c->queue_capacity = 0;
   c->timeout_s = 0.0;
   c->stream = nullptr;
@@ -186,6 +187,8 @@ static void graph_free(atos_graph g) {
   cudaFree(w.u32a);
   cudaFree(w.f32a);
   cudaFree(w.f32b);
+  cudaFree(w.f64a);
+  cudaFree(w.f64b);
   cudaFree(w.front[0]);
   cudaFree(w.front[1]);
   cudaFree(w.fcount);
@@ -268,6 +271,7 @@ atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, ui
       CK(cudaMemsetAsync(w.ring, 0, std::min<uint64_t>(w.dirty, cap) * sizeof(uint64_t), s));
       w.dirty = 0;
     }
+    w.dirty = cap;  // unknown until this run finishes cleanly (finish_stats narrows it)
   }
   (void)n_local;
   return ATOS_OK;
@@ -305,7 +309,8 @@ struct LaunchCtx {
   atos_config cfg;
   cudaStream_t s;
   GraphView gv;
-  int64_t launches = 0;
+  int64_t launches = 0;       // every kernel launched by the call up to the run's end
+  int64_t post_launches = 0;  // launched after the run (reductions, conversions)
   int64_t rounds = 0;
   std::chrono::steady_clock::time_point t0;
 };
@@ -316,10 +321,21 @@ static atos_status set_smem(K kern, size_t smem) {
   return ATOS_OK;
 }
 
+// Warp/thread workers stage their claimed items in shared memory (4 B per item,
+// FETCH per warp worker, 32*FETCH per thread-worker warp); shrink the block so
+// the staging buffer fits in 227 KB.  CTA workers keep cta_threads.
+static int clamp_threads(int W, int F, int T) {
+  if (W == W_CTA) return T;
+  const size_t per_warp = (W == W_WARP ? (size_t)F : 32 * (size_t)F) * 4;
+  int max_warps = (int)((227 * 1024) / per_warp);
+  if (max_warps < 1) max_warps = 1;
+  return std::min(T, max_warps * 32);
+}
+
 template <class P, class App, int W>
 static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q) {
   auto kern = k_persistent<P, App, W>;
-  const int F = c.cfg.fetch_size, T = c.cfg.cta_threads;
+  const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads);
   const size_t smem = worker_smem_bytes<P>(W, F, T);
   if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
   CKS(set_smem(kern, smem));
@@ -355,7 +371,7 @@ static atos_status host_timeout(LaunchCtx& c) {
 template <class P, class App, int W>
 static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0) {
   auto kern = k_discrete<P, App, W>;
-  const int F = c.cfg.fetch_size, T = c.cfg.cta_threads;
+  const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads);
   const size_t smem = worker_smem_bytes<P>(W, F, T);
   if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
   CKS(set_smem(kern, smem));
@@ -445,14 +461,14 @@ static atos_status finish_stats(LaunchCtx& c, atos_stats* st, bool bsp) {
   Workspace& w = c.g->ws;
   CK(cudaEventRecord(w.ev[2], c.s));
   CKS(read_ctl(c.g, c.s));
-  if (!bsp) w.dirty = std::max<uint64_t>(w.dirty, std::min<uint64_t>(w.h_ctl->tail.v, w.cap));
+  if (!bsp) w.dirty = std::min<uint64_t>(w.h_ctl->tail.v, w.cap);
   if (st) {
     float ms = 0, kms = 0;
     CK(cudaEventElapsedTime(&ms, w.ev[0], w.ev[2]));
     CK(cudaEventElapsedTime(&kms, w.ev[1], w.ev[2]));
     st->ms = ms;
     st->kernel_ms = kms;
-    st->kernel_launches = c.launches;
+    st->kernel_launches = c.launches + c.post_launches;
     st->tasks_popped = (int64_t)w.h_ctl->stats[0].v;
     st->tasks_pushed = (int64_t)w.h_ctl->stats[1].v;
     st->edges_processed = (int64_t)w.h_ctl->stats[2].v;
@@ -507,6 +523,7 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
   k_bfs_init<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, n, src);
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : 1, w.ring, bsp ? -1 : src);
   CK(cudaGetLastError());
+  c.launches += 2;
   CK(cudaEventRecord(w.ev[1], c.s));
   BfsApp app{w.u32a, c.cfg.bfs_filter};
   using P = EdgeMapPolicy<BfsApp>;
@@ -534,6 +551,53 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
 }
 
 // ------------------------------------------------------------------ PageRank
+template <class R>
+static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha, float eps) {
+  atos_graph g = c.g;
+  Workspace& w = g->ws;
+  const int64_t n = g->n;
+  const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
+  CK(cudaEventRecord(w.ev[0], c.s));
+  // a2: rank = 1 - alpha ; residue seeded by one synchronous push (R4) ; all vertices enqueued (P:487)
+  k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rank, n, 1.0 - (double)alpha);
+  k_fill<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, R(0));
+  k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
+  {
+    PrInitAppT<R> ia{res, (R)(1.0 - (double)alpha) * (R)alpha};
+    LaunchCtx ci = c;
+    ci.cfg.worker = ATOS_WORKER_CTA;
+    CKS((bsp_step_w<EdgeMapPolicy<PrInitAppT<R>>, PrInitAppT<R>, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr, nullptr,
+                                                                       256, nullptr)));
+  }
+  if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
+  CK(cudaGetLastError());
+  c.launches += bsp ? 4 : 5;
+  CK(cudaEventRecord(w.ev[1], c.s));
+  PrAppT<R> app{rank, res, (R)alpha, (R)eps};
+  if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
+    CKS(run_persistent<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg)));
+  } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
+    CKS(run_discrete<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg), (uint64_t)n));
+  } else {
+    // Alg. 3: push kernel over the frontier, then filter kernel over all vertices
+    PrBspAppT<R> bapp{app};
+    uint64_t cnt = (uint64_t)n;
+    const uint32_t* in = nullptr;  // first frontier: all vertices (P:487)
+    int cur = 0;
+    while (cnt > 0) {
+      CKS(bsp_step<EdgeMapPolicy<PrBspAppT<R>>>(c, bapp, in, cnt, nullptr, nullptr));
+      CK(cudaMemsetAsync(w.fcount, 0, sizeof(unsigned long long), c.s));
+      k_pr_filter<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, (R)eps, w.front[cur], w.fcount);
+      CK(cudaGetLastError());
+      c.launches++;
+      CKS(bsp_read_count(c, w.fcount, cnt));
+      in = w.front[cur];
+      cur ^= 1;
+    }
+  }
+  return ATOS_OK;
+}
+
 extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const atos_config* cfg, float* rank_out,
                                      atos_stats* st) {
   LaunchCtx c;
@@ -547,62 +611,30 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   if (c.cfg.pr_activation == 1) return atos_set_error(ATOS_ERR_UNSUPPORTED, "Check_Size window activation not built");
   Workspace& w = g->ws;
   const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
+  const bool r64 = c.cfg.pr_residue_fp64 != 0;
   // at most 2 live copies per vertex (initial + one threshold crossing)
   CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)n, !bsp, c.s));
+  if (!bsp && (uint64_t)n > w.cap)
+    return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "queue_capacity %llu < n = %lld initial tasks",
+                          (unsigned long long)w.cap, (long long)n);
   CKS(ensure(w.f32a, w.f32a_n, (size_t)n));
-  CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
+  CKS(ensure(w.f64a, w.f64a_n, (size_t)n));
+  if (r64) CKS(ensure(w.f64b, w.f64b_n, (size_t)n));
+  else CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
   if (bsp) {
     CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
     CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
   }
-  if (!bsp && (uint64_t)n > w.cap)
-    return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "queue_capacity %llu < n = %lld initial tasks",
-                          (unsigned long long)w.cap, (long long)n);
-  float* rank = w.f32a;
-  float* res = w.f32b;
-  CK(cudaEventRecord(w.ev[0], c.s));
-  // a2: rank = 1 - alpha ; residue seeded by one synchronous push (R4) ; all vertices enqueued (P:487)
-  k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rank, n, 1.0f - alpha);
-  k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, 0.0f);
-  k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
-  {
-    PrInitApp ia{res, (1.0f - alpha) * alpha};
-    atos_config ic = c.cfg;
-    ic.worker = ATOS_WORKER_CTA;
-    LaunchCtx ci = c;
-    ci.cfg = ic;
-    CKS((bsp_step_w<EdgeMapPolicy<PrInitApp>, PrInitApp, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr, nullptr, 256, nullptr)));
-  }
-  if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
-  CK(cudaGetLastError());
-  CK(cudaEventRecord(w.ev[1], c.s));
-  PrApp app{rank, res, alpha, eps};
-  if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
-    CKS(run_persistent<EdgeMapPolicy<PrApp>>(c, app, make_queue(g, c.cfg)));
-  } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
-    CKS(run_discrete<EdgeMapPolicy<PrApp>>(c, app, make_queue(g, c.cfg), (uint64_t)n));
-  } else {
-    // Alg. 3: push kernel over the frontier, then filter kernel over all vertices
-    PrBspApp bapp{app};
-    uint64_t cnt = (uint64_t)n;
-    const uint32_t* in = nullptr;  // first frontier: all vertices (P:487)
-    int cur = 0;
-    while (cnt > 0) {
-      CKS(bsp_step<EdgeMapPolicy<PrBspApp>>(c, bapp, in, cnt, nullptr, nullptr));
-      CK(cudaMemsetAsync(w.fcount, 0, sizeof(unsigned long long), c.s));
-      k_pr_filter<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, eps, w.front[cur], w.fcount);
-      CK(cudaGetLastError());
-      c.launches++;
-      CKS(bsp_read_count(c, w.fcount, cnt));
-      in = w.front[cur];
-      cur ^= 1;
-    }
-  }
+  double* rank = w.f64a;
+  if (r64) CKS(pagerank_run<double>(c, w.f64b, rank, alpha, eps));
+  else CKS(pagerank_run<float>(c, w.f32b, rank, alpha, eps));
+  c.post_launches = st ? 2 : 1;
   CKS(finish_stats(c, st, bsp));
   if (st) {
     unsigned int* mb = reinterpret_cast<unsigned int*>(g->d_scratch) + 8;
     CK(cudaMemsetAsync(mb, 0, sizeof(unsigned int), c.s));
-    k_max_f32<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, mb);
+    if (r64) k_max_f32<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.f64b, n, mb);
+    else k_max_f32<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.f32b, n, mb);
     unsigned int hb = 0;
     CK(cudaMemcpyAsync(&hb, mb, sizeof hb, cudaMemcpyDeviceToHost, c.s));
     CK(cudaStreamSynchronize(c.s));
@@ -610,7 +642,9 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
     std::memcpy(&f, &hb, sizeof f);
     st->max_residue = f;
   }
-  CKS(copy_out(rank_out, rank, (size_t)n * sizeof(float), c.s));
+  k_f64_to_f32<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rank, w.f32a, n);
+  CK(cudaGetLastError());
+  CKS(copy_out(rank_out, w.f32a, (size_t)n * sizeof(float), c.s));
   CK(cudaStreamSynchronize(c.s));
   return ATOS_OK;
 }
@@ -647,6 +681,7 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
   if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);  // ASSIGN(v), id order (R22)
   CK(cudaGetLastError());
+  c.launches += bsp ? 3 : 4;
   CK(cudaEventRecord(w.ev[1], c.s));
   GcApp app{color, pend};
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
@@ -667,6 +702,7 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
       cur ^= 1;
     }
   }
+  c.post_launches = 1;
   CKS(finish_stats(c, st, bsp));
   int* mx = reinterpret_cast<int*>(g->d_scratch) + 12;
   CK(cudaMemsetAsync(mx, 0xFF, sizeof(int), c.s));

@@ -19,6 +19,10 @@ struct Workspace {
   size_t f32a_n = 0;
   float* f32b = nullptr;  // PR residue
   size_t f32b_n = 0;
+  double* f64a = nullptr;  // PR rank (fp64 accumulation)
+  size_t f64a_n = 0;
+  double* f64b = nullptr;  // PR residue when pr_residue_fp64
+  size_t f64b_n = 0;
   uint32_t* front[2] = {nullptr, nullptr};
   size_t front_n[2] = {0, 0};
   unsigned long long* fcount = nullptr;

@@ -52,33 +52,47 @@ struct BfsApp {
 // Push PageRank (Alg. 4 body; dangling R5; activation R6):
 // r = atomicExch(res[v], 0); rank[v] += r; c = alpha r / deg(v);
 // per edge: old = atomicAdd(res[w], c); push w iff old <= eps < old + c.
-struct PrApp {
-  float* rank;
-  float* res;
-  float alpha, eps;
-  using Payload = float;
+// rank accumulates in fp64 (a per-pop cost): a hub receives 10^4+ pops.
+// Residues are R = float (default: 4 B per edge push) or double
+// (atos_config.pr_residue_fp64): a vertex whose claimed task waits long (thread
+// workers with a large FETCH) accumulates a residue of O(10) and fp32 then
+// absorbs pushes below its ulp — measured 6.6e-4 of max(x*) on RMAT-16.
+__device__ __forceinline__ float atomic_take(float* p) { return atomicExch(p, 0.0f); }
+__device__ __forceinline__ double atomic_take(double* p) {
+  return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long*>(p), 0ull));
+}
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+template <class R>
+struct PrAppT {
+  double* rank;
+  R* res;
+  R alpha, eps;
+  using Payload = R;
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
     e0 = ld_nc_s64(g.off + v);
     e1 = ld_nc_s64(g.off + v + 1);
-    const float r = atomicExch(res + v, 0.0f);
-    if (r == 0.0f) return false;
-    atomicAdd(rank + v, r);
+    const R r = atomic_take(res + v);
+    if (r == R(0)) return false;
+    atomicAdd(rank + v, (double)r);
     if (e1 == e0) return false;
-    p = __fdiv_rn(__fmul_rn(alpha, r), (float)(e1 - e0));
+    p = alpha * r / (R)(e1 - e0);
     return true;
   }
   __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
-    const float old = atomicAdd(res + w, c);
-    return old <= eps && __fadd_rn(old, c) > eps;
+    const R old = atomicAdd(res + w, c);
+    return old <= eps && add_rn(old, c) > eps;
   }
 };
 
 // BSP PageRank push kernel body (Alg. 3 lines 11-16): same push
 // but the frontier is rebuilt by the filter kernel, so nothing is appended.
-struct PrBspApp {
-  PrApp base;
-  using Payload = float;
+template <class R>
+struct PrBspAppT {
+  PrAppT<R> base;
+  using Payload = R;
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
     return base.begin(v, g, e0, e1, p);

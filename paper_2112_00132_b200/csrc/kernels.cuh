@@ -274,6 +274,7 @@ __global__ void k_ring_prefill(uint64_t* ring, int64_t n, uint32_t tag) {
 __global__ void k_ctl_init(QueueCtl* ctl, uint64_t tail, uint64_t* ring, int64_t src_item) {
   ctl->head.v = 0;
   ctl->tail.v = tail;
+  ctl->count.v = tail;
   ctl->processed.v = 0;
   ctl->abort.v = 0;
   ctl->high_water.v = tail;
@@ -289,15 +290,16 @@ __global__ void k_bfs_init(uint32_t* dist, int64_t n, int64_t src) {
 
 // PR residue seeding (reading R4 of Alg. 3 lines 5-7): the edge-map of an
 // app that pushes c = (1-a) a / deg(v) to every out-neighbour, no activation.
-struct PrInitApp {
-  float* res;
-  float c0;  // (1 - alpha) * alpha
-  using Payload = float;
+template <class R>
+struct PrInitAppT {
+  R* res;
+  R c0;  // (1 - alpha) * alpha
+  using Payload = R;
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1, Payload& p) const {
     e0 = ld_nc_s64(g.off + v);
     e1 = ld_nc_s64(g.off + v + 1);
     if (e1 == e0) return false;
-    p = __fdiv_rn(c0, (float)(e1 - e0));
+    p = c0 / (R)(e1 - e0);
     return true;
   }
   __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
@@ -306,8 +308,14 @@ struct PrInitApp {
   }
 };
 
+__global__ void k_f64_to_f32(const double* a, float* b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+
 // BSP PageRank filter kernel (Alg. 3 lines 18-22): residue > eps -> frontier
-__global__ void k_pr_filter(const float* res, int64_t n, float eps, uint32_t* out, unsigned long long* count) {
+template <class R>
+__global__ void k_pr_filter(const R* res, int64_t n, R eps, uint32_t* out, unsigned long long* count) {
   ArraySink sink{out, count};
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; b < n; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = b + lane_id();
@@ -317,9 +325,10 @@ __global__ void k_pr_filter(const float* res, int64_t n, float eps, uint32_t* ou
 }
 
 // max reduction helpers for stats
-__global__ void k_max_f32(const float* a, int64_t n, unsigned int* out_bits) {
+template <class R>
+__global__ void k_max_f32(const R* a, int64_t n, unsigned int* out_bits) {
   float m = 0.f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) m = fmaxf(m, a[i]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) m = fmaxf(m, (float)a[i]);
   for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL_MASK, m, d));
   if (lane_id() == 0) atomicMax(out_bits, __float_as_uint(m));  // m >= 0 so bit order == value order
 }
