@@ -82,7 +82,7 @@ typedef struct {
   double ms;                /* device time of init + run (CUDA events on cfg->stream)     */
   double kernel_ms;         /* device time of the hot-path kernels alone (sum)            */
   int64_t kernel_launches;  /* every kernel this call launched (init + hot path + reductions) */
-  int64_t tasks_popped;     /* queue items processed (vertices / colour tasks)            */
+  int64_t tasks_popped;     /* vertex / colour tasks processed (excludes chunk tasks)     */
   int64_t tasks_pushed;     /* items pushed after init                                    */
   int64_t edges_processed;  /* edge visits (BFS relax attempts, PR edge pushes, GC scans) */
   int64_t rounds;           /* discrete/BSP rounds, multi-GPU exchange rounds             */
@@ -91,6 +91,7 @@ typedef struct {
   int32_t num_colors;       /* atos_color: colours used                                   */
   int32_t _pad;
   double max_residue;       /* atos_pagerank: max residue at return (must be <= eps)      */
+  int64_t chunk_tasks;      /* hub edge-chunk tasks processed (persistent CTA workers)    */
 } atos_stats;
 
 /* Fill *cfg with defaults: persistent, CTA worker, 256 threads, fetch 256,

@@ -60,7 +60,7 @@ class CStats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("tasks_popped", ctypes.c_int64),
                 ("tasks_pushed", ctypes.c_int64), ("edges_processed", ctypes.c_int64), ("rounds", ctypes.c_int64),
                 ("queue_high_water", ctypes.c_int64), ("bytes_sent", ctypes.c_int64), ("num_colors", ctypes.c_int32),
-                ("_pad", ctypes.c_int32), ("max_residue", ctypes.c_double)]
+                ("_pad", ctypes.c_int32), ("max_residue", ctypes.c_double), ("chunk_tasks", ctypes.c_int64)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k not in ("struct_size", "_pad")}

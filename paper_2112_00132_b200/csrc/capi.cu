@@ -192,6 +192,7 @@ static void graph_free(atos_graph g) {
   cudaFree(w.front[0]);
   cudaFree(w.front[1]);
   cudaFree(w.fcount);
+  cudaFree(w.chunks);
   if (w.h_ctl) cudaFreeHost(w.h_ctl);
   for (auto& e : w.ev)
     if (e) cudaEventDestroy(e);
@@ -336,6 +337,16 @@ template <class P, class App, int W>
 static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q) {
   auto kern = k_persistent<P, App, W>;
   const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads);
+  Queue qq = q;
+  if (W == W_CTA && P::kSplit) {
+    Workspace& w = c.g->ws;
+    if (!w.chunks) {
+      w.chunk_cap = 1ull << 20;
+      CK(cudaMalloc(&w.chunks, w.chunk_cap * sizeof(Chunk)));
+    }
+    qq.chunks = w.chunks;
+    qq.chunk_mask = w.chunk_cap - 1;
+  }
   const size_t smem = worker_smem_bytes<P>(W, F, T);
   if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
   CKS(set_smem(kern, smem));
@@ -344,7 +355,7 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
   if (per_sm < 1) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "kernel cannot be resident with %d threads", T);
   int blocks = per_sm * c.g->sms;
   if (c.cfg.num_blocks > 0) blocks = std::min(blocks, c.cfg.num_blocks);  // persistent: <= resident maximum
-  kern<<<blocks, T, smem, c.s>>>(app, c.gv, q, F);
+  kern<<<blocks, T, smem, c.s>>>(app, c.gv, qq, F);
   CK(cudaGetLastError());
   c.launches++;
   return ATOS_OK;
@@ -469,7 +480,8 @@ static atos_status finish_stats(LaunchCtx& c, atos_stats* st, bool bsp) {
     st->ms = ms;
     st->kernel_ms = kms;
     st->kernel_launches = c.launches + c.post_launches;
-    st->tasks_popped = (int64_t)w.h_ctl->stats[0].v;
+    st->chunk_tasks = (int64_t)w.h_ctl->chunk_done.v;
+    st->tasks_popped = (int64_t)w.h_ctl->stats[0].v - st->chunk_tasks;
     st->tasks_pushed = (int64_t)w.h_ctl->stats[1].v;
     st->edges_processed = (int64_t)w.h_ctl->stats[2].v;
     st->rounds = c.rounds;

@@ -26,6 +26,8 @@ struct Workspace {
   uint32_t* front[2] = {nullptr, nullptr};
   size_t front_n[2] = {0, 0};
   unsigned long long* fcount = nullptr;
+  atos::Chunk* chunks = nullptr;  // hub chunk table
+  uint64_t chunk_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 

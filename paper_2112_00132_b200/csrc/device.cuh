@@ -15,8 +15,8 @@
 //    (items fully processed, including their pushes) are 64-bit counters, each
 //    on its own 128-byte line.
 //  * push (a3): warp-aggregated — __ballot_sync/__popc, ONE atomicAdd(tail)
-//    per warp, each lane writes its slot with st.release.gpu, then the leader
-//    publishes the batch with one red.release.add(count).
+//    per warp (plus one red.add(count) that publishes the batch), then each
+//    lane writes its slot (see q_store_slot for the ordering argument).
 //  * pop (a4): the worker leader reserves n = min(FETCH, count) items from a
 //    signed `count` of published items (fetch-and-add, excess returned), then
 //    claims positions with atomicAdd(head, n).  Reservations never exceed
@@ -78,8 +78,8 @@ __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ void st_relaxed_s32(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void red_add_release_s64(uint64_t* p, int64_t v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void red_add_relaxed_s64(uint64_t* p, int64_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void atom_add_release_u64(uint64_t* p, uint64_t v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -128,6 +128,8 @@ struct QueueCtl {
   Line64 processed;
   Line64 abort;         // ABORT_* code (u32 in .v)
   Line64 high_water;    // max observed tail - head
+  Line64 chunk_tail;    // hub chunk table: entries allocated
+  Line64 chunk_done;    // hub chunk table: entries consumed
   Line64 stats[4];      // popped, pushed, edges, spare
   Line64 aux[4];        // app-specific counters (e.g. PR check cursor, colours)
 };
@@ -141,6 +143,18 @@ struct Queue {
   uint64_t deadline;    // %globaltimer deadline (ns); 0 = none (armed by q_arm)
   uint64_t timeout_ns;  // 0 = no watchdog
   uint64_t head_floor;  // discrete rounds: every position < head_floor is claimed
+  struct Chunk* chunks; // hub chunk table (persistent CTA edge-map workers); nullptr = no splitting
+  uint64_t chunk_mask;  // table capacity - 1
+};
+
+// A slice [e0, e1) of a hub's adjacency list, queued as its own task
+// (item = CHUNK_BIT | table index).  payload = the app payload computed when
+// the hub was popped (BFS: dist+1, PR: alpha r / deg).
+constexpr uint32_t CHUNK_BIT = 0x80000000u;
+struct Chunk {
+  uint64_t payload;
+  int64_t e0, e1;
+  uint64_t pad;
 };
 
 __device__ __forceinline__ bool q_aborted(const Queue& q) {
@@ -181,7 +195,13 @@ __device__ __forceinline__ bool q_store_slot(const Queue& q, uint64_t p, uint32_
       ns = ns < 1024 ? ns * 2 : ns;
     }
   }
-  st_release_u64(slot, ((uint64_t)(2u * lap + 1u) << 32) | item);
+  // Relaxed (strong, L2) store: every push predicate is computed from the
+  // RETURNED value of the atomic that produced the state its consumer reads
+  // (BFS atomicMin, PR atomicAdd, GC atomicExch after __threadfence), so that
+  // atomic is performed at L2 — the point of coherence — before this store
+  // issues.  A st.release here cost a MEMBAR+ERRBAR per push (19% of BFS
+  // stall samples, profiles/r01_bfs_rmat24_v1).
+  st_relaxed_u64(slot, ((uint64_t)(2u * lap + 1u) << 32) | item);
   return true;
 }
 
@@ -216,11 +236,12 @@ __device__ __forceinline__ uint32_t q_warp_push(const Queue& q, bool pred, uint3
   const int leader = __ffs(mask) - 1;
   const uint32_t cnt = __popc(mask);
   unsigned long long base = 0;
-  if ((int)lane == leader) base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)cnt);
+  if ((int)lane == leader) {
+    base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)cnt);
+    red_add_relaxed_s64(&q.ctl->count.v, (int64_t)cnt);  // publish (consumers spin on slot tags)
+  }
   base = __shfl_sync(FULL_MASK, base, leader);
   if (pred) q_store_slot(q, base + __popc(mask & lanemask_lt()), item);
-  __syncwarp();
-  if ((int)lane == leader) red_add_release_s64(&q.ctl->count.v, (int64_t)cnt);  // publish
   return cnt;
 }
 
@@ -234,12 +255,21 @@ __device__ __forceinline__ uint32_t q_active_push(const Queue& q, bool pred, uin
   const int leader = __ffs(mask) - 1;
   const uint32_t cnt = __popc(mask);
   unsigned long long base = 0;
-  if ((int)lane == leader) base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)cnt);
+  if ((int)lane == leader) {
+    base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)cnt);
+    red_add_relaxed_s64(&q.ctl->count.v, (int64_t)cnt);
+  }
   base = __shfl_sync(act, base, leader);
   if (pred) q_store_slot(q, base + __popc(mask & lanemask_lt()), item);
-  __syncwarp(act);
-  if ((int)lane == leader) red_add_release_s64(&q.ctl->count.v, (int64_t)cnt);  // publish
   return cnt;
+}
+
+// Single-thread push of k items item_of(j), j < k (hub chunk tasks).
+template <class F>
+__device__ __forceinline__ void q_thread_push(const Queue& q, uint32_t k, F item_of) {
+  const unsigned long long base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)k);
+  red_add_relaxed_s64(&q.ctl->count.v, (int64_t)k);
+  for (uint32_t j = 0; j < k; ++j) q_store_slot(q, base + j, item_of(j));
 }
 
 // Single-thread pop (a4): claim up to `want` published items with two

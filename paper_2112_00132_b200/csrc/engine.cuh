@@ -226,17 +226,72 @@ __device__ __forceinline__ int lbs_find(const int64_t* pre, int n, int64_t e) {
 
 constexpr int LBS_UNROLL = 4;
 
+// Hub splitting (persistent CTA workers): a popped vertex with more than
+// SPLIT_DEG edges keeps its first CHUNK_EDGES edges and publishes the rest as
+// CHUNK_EDGES-sized chunk tasks on the same queue, so all SMs expand a hub in
+// parallel instead of one CTA walking it serially while the rest of the GPU
+// speculates on depths the hub has not yet fixed (the measured source of
+// RMAT-24 BFS overwork).
+constexpr int64_t CHUNK_EDGES = 2048;
+constexpr int64_t SPLIT_DEG = 2 * CHUNK_EDGES;
+
+template <class P>
+__device__ __forceinline__ uint64_t pack_payload(P p) {
+  uint64_t u = 0;
+  memcpy(&u, &p, sizeof(P));
+  return u;
+}
+template <class P>
+__device__ __forceinline__ P unpack_payload(uint64_t u) {
+  P p;
+  memcpy(&p, &u, sizeof(P));
+  return p;
+}
+
+template <class Src>
+__device__ __forceinline__ const Queue* chunk_queue(const Src&) { return nullptr; }
+__device__ __forceinline__ const Queue* chunk_queue(const RingSrc& s) { return s.q.chunks ? &s.q : nullptr; }
+
 // Process batch items [0, n) with the whole CTA.  Every thread must call.
 template <class App, class Src, class Sink>
 __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, const Src& src, const Sink& sink,
                                           uint32_t n, CtaSmem<typename App::Payload>& sm, LocalStats& st) {
   using Payload = typename App::Payload;
   const int T = blockDim.x, tid = threadIdx.x;
+  const Queue* cq = chunk_queue(src);
   for (int i = tid; i < (int)n; i += T) {
     uint32_t item = 0;
     int64_t e0 = 0, e1 = 0;
     Payload p{};
-    bool ok = src.get(i, item) && app.begin(item, g, e0, e1, p);
+    bool ok = src.get(i, item);
+    if (ok && cq && (item & CHUNK_BIT)) {
+      const Chunk* c = cq->chunks + (item & ~CHUNK_BIT);
+      e0 = c->e0;
+      e1 = c->e1;
+      p = unpack_payload<Payload>(c->payload);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_done.v), 1ull);
+    } else if (ok) {
+      ok = app.begin(item, g, e0, e1, p);
+      if (ok && cq && e1 - e0 > SPLIT_DEG) {
+        const uint32_t k = (uint32_t)((e1 - e0 - 1) / CHUNK_EDGES);  // chunks beyond the first
+        const unsigned long long base =
+            atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_tail.v), (unsigned long long)k);
+        if (base + k - ld_relaxed_u64(&cq->ctl->chunk_done.v) > cq->chunk_mask + 1) {
+          q_raise(*cq, ABORT_OVERFLOW);
+        } else {
+          const uint64_t pb = pack_payload(p);
+          for (uint32_t j = 0; j < k; ++j) {
+            Chunk* c = cq->chunks + ((base + j) & cq->chunk_mask);
+            c->payload = pb;
+            c->e0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
+            c->e1 = min(e1, e0 + CHUNK_EDGES * (int64_t)(j + 2));
+          }
+          __threadfence();  // chunk entries visible before their tasks
+          q_thread_push(*cq, k, [&](uint32_t j) { return CHUNK_BIT | (uint32_t)((base + j) & cq->chunk_mask); });
+          e1 = e0 + CHUNK_EDGES;
+        }
+      }
+    }
     sm.e0[i] = e0;
     sm.pre[i] = ok ? e1 - e0 : 0;
     sm.pay[i] = p;

@@ -18,6 +18,7 @@ __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { re
 // ---------------------------------------------------------------- policies
 template <class App>
 struct EdgeMapPolicy {
+  static constexpr bool kSplit = true;  // CTA workers split hubs into chunk tasks
   using Payload = typename App::Payload;
   static __host__ __device__ size_t smem_bytes(int F) { return cta_smem_bytes<Payload>(F); }
   template <class Src, class Sink>
@@ -40,6 +41,7 @@ struct EdgeMapPolicy {
 
 template <int MODE>
 struct GcPolicy {
+  static constexpr bool kSplit = false;
   static __host__ __device__ size_t smem_bytes(int F) { return gc_cta_smem_bytes(F); }
   template <class Src, class Sink>
   static __device__ __forceinline__ void cta(const GcApp& app, const GraphView& g, const Src& src, const Sink& sink,
@@ -278,6 +280,8 @@ __global__ void k_ctl_init(QueueCtl* ctl, uint64_t tail, uint64_t* ring, int64_t
   ctl->processed.v = 0;
   ctl->abort.v = 0;
   ctl->high_water.v = tail;
+  ctl->chunk_tail.v = 0;
+  ctl->chunk_done.v = 0;
   for (int i = 0; i < 4; ++i) { ctl->stats[i].v = 0; ctl->aux[i].v = 0; }
   if (src_item >= 0) ring[0] = (1ull << 32) | (uint64_t)(uint32_t)src_item;
 }
