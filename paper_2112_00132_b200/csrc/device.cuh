@@ -64,6 +64,28 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// relaxed at CTA scope: may hit in L1 and return a stale (older) value; used
+// only where a stale value is safe (BFS probe: dist only decreases).
+__device__ __forceinline__ uint32_t ld_relaxed_cta_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.cta.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32_nc(const uint32_t* p) {  // no compiler memory clobber
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_cg_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_cg_s64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -211,12 +233,17 @@ __device__ __forceinline__ bool q_load_slot(const Queue& q, uint64_t p, uint32_t
   uint64_t* slot = q.ring + (p & q.mask);
   const uint32_t lap = (uint32_t)(p >> q.log2cap);
   const uint32_t want = 2u * lap + 1u;
-  uint64_t w = ld_acquire_u64(slot);
+  // Relaxed (strong, L2) load: everything the consumer then reads about the
+  // item is addressed THROUGH the item (dist[v], res[v], off[v], chunk[i]) and
+  // read from L2, so it cannot be issued before this load returns.  An
+  // ld.acquire here adds CCTL.IVALL (L1 invalidate) per item, which would also
+  // defeat the L1-cached BFS filter probes.
+  uint64_t w = ld_relaxed_u64(slot);
   if ((uint32_t)(w >> 32) != want) {
     unsigned ns = 16;
     for (;;) {
       __nanosleep(ns);
-      w = ld_acquire_u64(slot);
+      w = ld_relaxed_u64(slot);
       if ((uint32_t)(w >> 32) == want) break;
       if (q_aborted(q) || q_timed_out(q)) return false;
       ns = ns < 256 ? ns * 2 : ns;
@@ -262,6 +289,32 @@ __device__ __forceinline__ uint32_t q_active_push(const Queue& q, bool pred, uin
   base = __shfl_sync(act, base, leader);
   if (pred) q_store_slot(q, base + __popc(mask & lanemask_lt()), item);
   return cnt;
+}
+
+// Warp-collective push of up to U items per lane with ONE atomicAdd on tail.
+template <int U>
+__device__ __forceinline__ uint32_t q_warp_push_multi(const Queue& q, const bool (&pred)[U], const uint32_t (&item)[U]) {
+  unsigned m[U];
+  uint32_t total = 0;
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    m[k] = __ballot_sync(FULL_MASK, pred[k]);
+    total += __popc(m[k]);
+  }
+  if (total == 0) return 0;
+  unsigned long long base = 0;
+  if (lane_id() == 0) {
+    base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)total);
+    red_add_relaxed_s64(&q.ctl->count.v, (int64_t)total);
+  }
+  base = __shfl_sync(FULL_MASK, base, 0);
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    if (pred[k]) q_store_slot(q, base + __popc(m[k] & lt), item[k]);
+    base += __popc(m[k]);
+  }
+  return total;
 }
 
 // Single-thread push of k items item_of(j), j < k (hub chunk tasks).

@@ -36,6 +36,16 @@ struct BfsApp {
   uint32_t* dist;
   int filter;
   using Payload = uint32_t;
+  using Probe = uint32_t;
+  // Two-phase edge: all probes of a thread's UNROLL edges are issued before
+  // any atomic (memory-level parallelism).  The probe may hit a stale L1 copy
+  // (>= the current value): it only lets through atomics that turn out not to
+  // improve, never suppresses one that would.
+  __device__ __forceinline__ Probe probe(uint32_t w) const { return filter ? ld_relaxed_cta_u32(dist + w) : 0xFFFFFFFFu; }
+  __device__ __forceinline__ bool commit(Payload nd, uint32_t w, Probe pr) const {
+    if (nd >= pr) return false;
+    return nd < atomicMin(dist + w, nd);
+  }
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
     e0 = ld_nc_s64(g.off + v);
@@ -85,6 +95,9 @@ struct PrAppT {
     const R old = atomicAdd(res + w, c);
     return old <= eps && add_rn(old, c) > eps;
   }
+  using Probe = int;
+  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
 };
 
 // BSP PageRank push kernel body (Alg. 3 lines 11-16): same push
@@ -101,6 +114,9 @@ struct PrBspAppT {
     atomicAdd(base.res + w, c);
     return false;
   }
+  using Probe = int;
+  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
 };
 
 // ------------------------------------------------------- sources / sinks ---
@@ -120,6 +136,10 @@ struct ArraySrc {
 
 struct RingSink {
   Queue q;
+  template <int U>
+  __device__ __forceinline__ uint32_t warp_push_multi(const bool (&pred)[U], const uint32_t (&item)[U]) const {
+    return q_warp_push_multi<U>(q, pred, item);
+  }
   __device__ __forceinline__ uint32_t warp_push(bool pred, uint32_t item) const { return q_warp_push(q, pred, item); }
   __device__ __forceinline__ uint32_t active_push(bool pred, uint32_t item) const { return q_active_push(q, pred, item); }
 };
@@ -127,6 +147,13 @@ struct RingSink {
 struct ArraySink {
   uint32_t* out;
   unsigned long long* count;
+  template <int U>
+  __device__ __forceinline__ uint32_t warp_push_multi(const bool (&pred)[U], const uint32_t (&item)[U]) const {
+    uint32_t t = 0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) t += warp_push(pred[k], item[k]);
+    return t;
+  }
   __device__ __forceinline__ uint32_t warp_push(bool pred, uint32_t item) const {
     const unsigned mask = __ballot_sync(FULL_MASK, pred);
     if (!mask) return 0;
@@ -224,6 +251,15 @@ __device__ __forceinline__ int lbs_find(const int64_t* pre, int n, int64_t e) {
   return lo;
 }
 
+// largest i in [lo, hi) with pre[i] <= e, given pre[lo] <= e < pre[hi]
+__device__ __forceinline__ int lbs_find_range(const int64_t* pre, int lo, int hi, int64_t e) {
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (pre[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 constexpr int LBS_UNROLL = 4;
 
 // Hub splitting (persistent CTA workers): a popped vertex with more than
@@ -266,9 +302,9 @@ __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, co
     bool ok = src.get(i, item);
     if (ok && cq && (item & CHUNK_BIT)) {
       const Chunk* c = cq->chunks + (item & ~CHUNK_BIT);
-      e0 = c->e0;
-      e1 = c->e1;
-      p = unpack_payload<Payload>(c->payload);
+      e0 = ld_cg_s64(&c->e0);  // L2: table entries are rewritten on wrap
+      e1 = ld_cg_s64(&c->e1);
+      p = unpack_payload<Payload>(ld_cg_u64(&c->payload));
       atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_done.v), 1ull);
     } else if (ok) {
       ok = app.begin(item, g, e0, e1, p);
@@ -303,22 +339,35 @@ __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, co
   const int64_t stride = (int64_t)T * LBS_UNROLL;
   uint32_t pushed = 0;
   for (int64_t eb = (int64_t)wid * 32 * LBS_UNROLL; eb < total; eb += stride) {
-    int32_t w[LBS_UNROLL];
+    // owners of this warp's first and last edge bound every lane's search
+    const int64_t elast = min(total, eb + 32 * LBS_UNROLL) - 1;
+    int bound = 0;
+    if (lane == 0) bound = lbs_find(sm.pre, (int)n, eb);
+    if (lane == 31) bound = lbs_find(sm.pre, (int)n, elast);
+    const int lo0 = __shfl_sync(FULL_MASK, bound, 0);
+    const int hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
+    uint32_t w[LBS_UNROLL];
     int idx[LBS_UNROLL];
+    int lo = lo0;
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k) {
       const int64_t e = eb + lane + 32 * k;
       idx[k] = -1;
+      w[k] = 0;
       if (e < total) {
-        idx[k] = lbs_find(sm.pre, (int)n, e);
-        w[k] = ld_stream_s32(g.col + sm.e0[idx[k]] + (e - sm.pre[idx[k]]));
+        lo = lbs_find_range(sm.pre, lo, hi, e);
+        idx[k] = lo;
+        w[k] = (uint32_t)ld_stream_s32(g.col + sm.e0[lo] + (e - sm.pre[lo]));
       }
     }
+    typename App::Probe pr[LBS_UNROLL];
 #pragma unroll
-    for (int k = 0; k < LBS_UNROLL; ++k) {
-      const bool act = idx[k] >= 0 && app.edge(sm.pay[idx[k]], (uint32_t)w[k]);
-      pushed += sink.warp_push(act, (uint32_t)w[k]);
-    }
+    for (int k = 0; k < LBS_UNROLL; ++k)
+      if (idx[k] >= 0) pr[k] = app.probe(w[k]);
+    bool act[LBS_UNROLL];
+#pragma unroll
+    for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.commit(sm.pay[idx[k]], w[k], pr[k]);
+    pushed += sink.template warp_push_multi<LBS_UNROLL>(act, w);
   }
   if (lane == 0) st.pushed += pushed;
   if (tid == 0) st.edges += total;
@@ -351,14 +400,15 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
     const int64_t vi = vb + lane;
     const bool v = vi < nv;
     int4 w4 = v ? ld_stream_v4(body + vi) : make_int4(0, 0, 0, 0);
-    bool a = v && app.edge(p, (uint32_t)w4.x);
-    bool b = v && app.edge(p, (uint32_t)w4.y);
-    bool c = v && app.edge(p, (uint32_t)w4.z);
-    bool d = v && app.edge(p, (uint32_t)w4.w);
-    pushed += sink.warp_push(a, (uint32_t)w4.x);
-    pushed += sink.warp_push(b, (uint32_t)w4.y);
-    pushed += sink.warp_push(c, (uint32_t)w4.z);
-    pushed += sink.warp_push(d, (uint32_t)w4.w);
+    const uint32_t w[4] = {(uint32_t)w4.x, (uint32_t)w4.y, (uint32_t)w4.z, (uint32_t)w4.w};
+    typename App::Probe pr[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v) pr[k] = app.probe(w[k]);
+    bool act[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) act[k] = v && app.commit(p, w[k], pr[k]);
+    pushed += sink.template warp_push_multi<4>(act, w);
   }
   {
     const int64_t e = a1 + lane;

@@ -221,6 +221,8 @@ struct IotaSrc {
   }
 };
 struct NullSink {
+  template <int U>
+  __device__ __forceinline__ uint32_t warp_push_multi(const bool (&)[U], const uint32_t (&)[U]) const { return 0; }
   __device__ __forceinline__ uint32_t warp_push(bool, uint32_t) const { return 0; }
   __device__ __forceinline__ uint32_t active_push(bool, uint32_t) const { return 0; }
 };
@@ -310,6 +312,9 @@ struct PrInitAppT {
     atomicAdd(res + w, c);
     return false;
   }
+  using Probe = int;
+  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
 };
 
 __global__ void k_f64_to_f32(const double* a, float* b, int64_t n) {
