@@ -15,6 +15,8 @@ struct Workspace {
   atos::QueueCtl* h_ctl = nullptr;  // pinned mirror
   uint32_t* u32a = nullptr;         // BFS dist / GC pend
   size_t u32a_n = 0;
+  uint32_t* u32b = nullptr;         // BFS done (expanded-at-depth)
+  size_t u32b_n = 0;
   float* f32a = nullptr;  // PR rank / GC colour
   size_t f32a_n = 0;
   float* f32b = nullptr;  // PR residue

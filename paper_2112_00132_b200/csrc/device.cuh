@@ -176,7 +176,7 @@ constexpr uint32_t CHUNK_BIT = 0x80000000u;
 struct Chunk {
   uint64_t payload;
   int64_t e0, e1;
-  uint64_t pad;
+  uint64_t v;  // the hub vertex
 };
 
 __device__ __forceinline__ bool q_aborted(const Queue& q) {

@@ -34,9 +34,13 @@ struct GraphView {
 // (strict, R2).
 struct BfsApp {
   uint32_t* dist;
+  uint32_t* done;  // done[v] = smallest depth at which v has been expanded (init MAX)
   int filter;
   using Payload = uint32_t;
   using Probe = uint32_t;
+  // Chunk task of v created with payload nd: still current iff dist[v]+1 == nd.
+  // If v improved since, a newer task of v exists and covers every edge.
+  __device__ __forceinline__ bool chunk_current(uint32_t v, Payload nd) const { return ld_relaxed_u32(dist + v) + 1u >= nd; }
   // Two-phase edge: all probes of a thread's UNROLL edges are issued before
   // any atomic (memory-level parallelism).  The probe may hit a stale L1 copy
   // (>= the current value): it only lets through atomics that turn out not to
@@ -46,12 +50,17 @@ struct BfsApp {
     if (nd >= pr) return false;
     return nd < atomicMin(dist + w, nd);
   }
+  // Expand v at its CURRENT depth d (R3) unless some task already expanded
+  // (or is expanding) v at depth <= d: a vertex pushed k times by k
+  // improvements is expanded at most once per distinct depth it is popped at.
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
     e0 = ld_nc_s64(g.off + v);
     e1 = ld_nc_s64(g.off + v + 1);
-    p = ld_relaxed_u32(dist + v) + 1u;
-    return e1 > e0;
+    const uint32_t d = ld_relaxed_u32(dist + v);
+    p = d + 1u;
+    if (e1 == e0) return false;
+    return atomicMin(done + v, d) > d;
   }
   __device__ __forceinline__ bool edge(Payload nd, uint32_t w) const {
     if (filter && nd >= ld_relaxed_u32(dist + w)) return false;
@@ -98,6 +107,7 @@ struct PrAppT {
   using Probe = int;
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
+  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
 };
 
 // BSP PageRank push kernel body (Alg. 3 lines 11-16): same push
@@ -117,6 +127,7 @@ struct PrBspAppT {
   using Probe = int;
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
+  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
 };
 
 // ------------------------------------------------------- sources / sinks ---
@@ -305,6 +316,7 @@ __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, co
       e0 = ld_cg_s64(&c->e0);  // L2: table entries are rewritten on wrap
       e1 = ld_cg_s64(&c->e1);
       p = unpack_payload<Payload>(ld_cg_u64(&c->payload));
+      ok = app.chunk_current((uint32_t)ld_cg_u64(&c->v), p);
       atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_done.v), 1ull);
     } else if (ok) {
       ok = app.begin(item, g, e0, e1, p);
@@ -319,6 +331,7 @@ __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, co
           for (uint32_t j = 0; j < k; ++j) {
             Chunk* c = cq->chunks + ((base + j) & cq->chunk_mask);
             c->payload = pb;
+            c->v = item;
             c->e0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
             c->e1 = min(e1, e0 + CHUNK_EDGES * (int64_t)(j + 2));
           }

@@ -288,10 +288,12 @@ __global__ void k_ctl_init(QueueCtl* ctl, uint64_t tail, uint64_t* ring, int64_t
   if (src_item >= 0) ring[0] = (1ull << 32) | (uint64_t)(uint32_t)src_item;
 }
 
-// BFS init: dist[:] = MAX, dist[src] = 0 (R1)
-__global__ void k_bfs_init(uint32_t* dist, int64_t n, int64_t src) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+// BFS init: dist[:] = MAX, dist[src] = 0 (R1); done[:] = MAX
+__global__ void k_bfs_init(uint32_t* dist, uint32_t* done, int64_t n, int64_t src) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     dist[i] = (i == src) ? 0u : 0xFFFFFFFFu;
+    done[i] = 0xFFFFFFFFu;
+  }
 }
 
 // PR residue seeding (reading R4 of Alg. 3 lines 5-7): the edge-map of an
@@ -314,7 +316,7 @@ struct PrInitAppT {
   }
   using Probe = int;
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
-  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
 };
 
 __global__ void k_f64_to_f32(const double* a, float* b, int64_t n) {
