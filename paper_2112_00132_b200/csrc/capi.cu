@@ -348,8 +348,10 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
     qq.chunks = w.chunks;
     qq.chunk_mask = w.chunk_cap - 1;
   }
-  const size_t smem = worker_smem_bytes<P>(W, F, T);
+  const size_t smem = worker_smem_bytes<P>(W, F, T, true);
   if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
+  if (W == W_CTA && P::kWarpSpecialised && T < 64)
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "persistent CTA workers need cta_threads >= 64 (1 queue warp + workers)");
   CKS(set_smem(kern, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));

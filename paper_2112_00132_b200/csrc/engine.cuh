@@ -299,64 +299,24 @@ template <class Src>
 __device__ __forceinline__ const Queue* chunk_queue(const Src&) { return nullptr; }
 __device__ __forceinline__ const Queue* chunk_queue(const RingSrc& s) { return s.q.chunks ? &s.q : nullptr; }
 
-// Process batch items [0, n) with the whole CTA.  Every thread must call.
-template <class App, class Src, class Sink>
-__device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, const Src& src, const Sink& sink,
-                                          uint32_t n, CtaSmem<typename App::Payload>& sm, LocalStats& st) {
-  using Payload = typename App::Payload;
-  const int T = blockDim.x, tid = threadIdx.x;
-  const Queue* cq = chunk_queue(src);
-  for (int i = tid; i < (int)n; i += T) {
-    uint32_t item = 0;
-    int64_t e0 = 0, e1 = 0;
-    Payload p{};
-    bool ok = src.get(i, item);
-    if (ok && cq && (item & CHUNK_BIT)) {
-      const Chunk* c = cq->chunks + (item & ~CHUNK_BIT);
-      e0 = ld_cg_s64(&c->e0);  // L2: table entries are rewritten on wrap
-      e1 = ld_cg_s64(&c->e1);
-      p = unpack_payload<Payload>(ld_cg_u64(&c->payload));
-      ok = app.chunk_current((uint32_t)ld_cg_u64(&c->v), p);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_done.v), 1ull);
-    } else if (ok) {
-      ok = app.begin(item, g, e0, e1, p);
-      if (ok && cq && e1 - e0 > SPLIT_DEG) {
-        const uint32_t k = (uint32_t)((e1 - e0 - 1) / CHUNK_EDGES);  // chunks beyond the first
-        const unsigned long long base =
-            atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_tail.v), (unsigned long long)k);
-        if (base + k - ld_relaxed_u64(&cq->ctl->chunk_done.v) > cq->chunk_mask + 1) {
-          q_raise(*cq, ABORT_OVERFLOW);
-        } else {
-          const uint64_t pb = pack_payload(p);
-          for (uint32_t j = 0; j < k; ++j) {
-            Chunk* c = cq->chunks + ((base + j) & cq->chunk_mask);
-            c->payload = pb;
-            c->v = item;
-            c->e0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
-            c->e1 = min(e1, e0 + CHUNK_EDGES * (int64_t)(j + 2));
-          }
-          __threadfence();  // chunk entries visible before their tasks
-          q_thread_push(*cq, k, [&](uint32_t j) { return CHUNK_BIT | (uint32_t)((base + j) & cq->chunk_mask); });
-          e1 = e0 + CHUNK_EDGES;
-        }
-      }
-    }
-    sm.e0[i] = e0;
-    sm.pre[i] = ok ? e1 - e0 : 0;
-    sm.pay[i] = p;
-  }
-  __syncthreads();
-  block_exclusive_scan(sm.pre, (int)n, sm.wsum);
-  const int64_t total = sm.pre[n];
-  const int wid = tid >> 5, lane = lane_id();
-  const int64_t stride = (int64_t)T * LBS_UNROLL;
+// Load-balancing search expansion of a prepared batch: pre[0..n] is the
+// exclusive prefix of the items' degrees, e0/pay their first edge and payload.
+// Warp `wi` of `nw` takes 32*UNROLL consecutive flattened edges per step; each
+// lane locates its edges' items by binary search bounded by the owners of the
+// warp's first and last edge, loads UNROLL columns, issues UNROLL probes, then
+// UNROLL commits, then ONE aggregated push.  Returns the pushes (per lane 0).
+template <class App, class Sink>
+__device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
+                                               const int64_t* e0s, const typename App::Payload* pay, int n,
+                                               int64_t total, int wi, int nw) {
+  const int lane = lane_id();
+  const int64_t stride = (int64_t)nw * 32 * LBS_UNROLL;
   uint32_t pushed = 0;
-  for (int64_t eb = (int64_t)wid * 32 * LBS_UNROLL; eb < total; eb += stride) {
-    // owners of this warp's first and last edge bound every lane's search
+  for (int64_t eb = (int64_t)wi * 32 * LBS_UNROLL; eb < total; eb += stride) {
     const int64_t elast = min(total, eb + 32 * LBS_UNROLL) - 1;
     int bound = 0;
-    if (lane == 0) bound = lbs_find(sm.pre, (int)n, eb);
-    if (lane == 31) bound = lbs_find(sm.pre, (int)n, elast);
+    if (lane == 0) bound = lbs_find(pre, n, eb);
+    if (lane == 31) bound = lbs_find(pre, n, elast);
     const int lo0 = __shfl_sync(FULL_MASK, bound, 0);
     const int hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
     uint32_t w[LBS_UNROLL];
@@ -368,9 +328,9 @@ __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, co
       idx[k] = -1;
       w[k] = 0;
       if (e < total) {
-        lo = lbs_find_range(sm.pre, lo, hi, e);
+        lo = lbs_find_range(pre, lo, hi, e);
         idx[k] = lo;
-        w[k] = (uint32_t)ld_stream_s32(g.col + sm.e0[lo] + (e - sm.pre[lo]));
+        w[k] = (uint32_t)ld_stream_s32(g.col + e0s[lo] + (e - pre[lo]));
       }
     }
     typename App::Probe pr[LBS_UNROLL];
@@ -379,9 +339,74 @@ __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, co
       if (idx[k] >= 0) pr[k] = app.probe(w[k]);
     bool act[LBS_UNROLL];
 #pragma unroll
-    for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.commit(sm.pay[idx[k]], w[k], pr[k]);
+    for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.commit(pay[idx[k]], w[k], pr[k]);
     pushed += sink.template warp_push_multi<LBS_UNROLL>(act, w);
   }
+  return pushed;
+}
+
+// Turn a popped queue item into an edge range + payload (a4 -> a5):
+// a chunk task reads its table entry; a vertex runs the app's begin() and, if
+// it is a hub and splitting is on (cq != nullptr), publishes all but its first
+// CHUNK_EDGES edges as chunk tasks.  Returns false if there is nothing to expand.
+template <class App>
+__device__ __forceinline__ bool prepare_item(const App& app, const GraphView& g, const Queue* cq, uint32_t item,
+                                             int64_t& e0, int64_t& e1, typename App::Payload& p) {
+  using Payload = typename App::Payload;
+  if (cq && (item & CHUNK_BIT)) {
+    const Chunk* c = cq->chunks + (item & ~CHUNK_BIT);
+    e0 = ld_cg_s64(&c->e0);  // L2: table entries are rewritten on wrap
+    e1 = ld_cg_s64(&c->e1);
+    p = unpack_payload<Payload>(ld_cg_u64(&c->payload));
+    const bool ok = app.chunk_current((uint32_t)ld_cg_u64(&c->v), p);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_done.v), 1ull);
+    return ok;
+  }
+  if (!app.begin(item, g, e0, e1, p)) return false;
+  if (cq && e1 - e0 > SPLIT_DEG) {
+    const uint32_t k = (uint32_t)((e1 - e0 - 1) / CHUNK_EDGES);  // chunks beyond the first
+    const unsigned long long base =
+        atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_tail.v), (unsigned long long)k);
+    if (base + k - ld_relaxed_u64(&cq->ctl->chunk_done.v) > cq->chunk_mask + 1) {
+      q_raise(*cq, ABORT_OVERFLOW);
+      return false;
+    }
+    const uint64_t pb = pack_payload(p);
+    for (uint32_t j = 0; j < k; ++j) {
+      Chunk* c = cq->chunks + ((base + j) & cq->chunk_mask);
+      c->payload = pb;
+      c->v = item;
+      c->e0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
+      c->e1 = min(e1, e0 + CHUNK_EDGES * (int64_t)(j + 2));
+    }
+    __threadfence();  // chunk entries visible before their tasks
+    q_thread_push(*cq, k, [&](uint32_t j) { return CHUNK_BIT | (uint32_t)((base + j) & cq->chunk_mask); });
+    e1 = e0 + CHUNK_EDGES;
+  }
+  return true;
+}
+
+// Process batch items [0, n) with the whole CTA.  Every thread must call.
+template <class App, class Src, class Sink>
+__device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, const Src& src, const Sink& sink,
+                                          uint32_t n, CtaSmem<typename App::Payload>& sm, LocalStats& st) {
+  using Payload = typename App::Payload;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const Queue* cq = chunk_queue(src);
+  for (int i = tid; i < (int)n; i += T) {
+    uint32_t item = 0;
+    int64_t e0 = 0, e1 = 0;
+    Payload p{};
+    bool ok = src.get(i, item) && prepare_item(app, g, cq, item, e0, e1, p);
+    sm.e0[i] = e0;
+    sm.pre[i] = ok ? e1 - e0 : 0;
+    sm.pay[i] = p;
+  }
+  __syncthreads();
+  block_exclusive_scan(sm.pre, (int)n, sm.wsum);
+  const int64_t total = sm.pre[n];
+  const int lane = lane_id();
+  const uint32_t pushed = lbs_expand(app, g, sink, sm.pre, sm.e0, sm.pay, (int)n, total, tid >> 5, T >> 5);
   if (lane == 0) st.pushed += pushed;
   if (tid == 0) st.edges += total;
   __syncthreads();

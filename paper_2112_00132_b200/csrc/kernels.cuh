@@ -7,6 +7,7 @@
 //   k_bsp         one launch per BSP step over an explicit frontier array
 //                 (Alg. 1/3/5), appending to an out-frontier.
 #pragma once
+#include "cta_ws.cuh"
 #include "gc.cuh"
 
 namespace atos {
@@ -19,8 +20,14 @@ __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { re
 template <class App>
 struct EdgeMapPolicy {
   static constexpr bool kSplit = true;  // CTA workers split hubs into chunk tasks
+  static constexpr bool kWarpSpecialised = true;
   using Payload = typename App::Payload;
   static __host__ __device__ size_t smem_bytes(int F) { return cta_smem_bytes<Payload>(F); }
+  static __host__ __device__ size_t ws_smem(int F) { return ws_smem_bytes<Payload>(F); }
+  static __device__ __forceinline__ void cta_persistent(const App& app, const GraphView& g, const Queue& q, int F,
+                                                        unsigned char* smem, LocalStats& st) {
+    cta_ws_persistent(app, g, q, F, smem, st);
+  }
   template <class Src, class Sink>
   static __device__ __forceinline__ void cta(const App& app, const GraphView& g, const Src& src, const Sink& sink,
                                              uint32_t n, unsigned char* smem, int F, LocalStats& st) {
@@ -42,6 +49,10 @@ struct EdgeMapPolicy {
 template <int MODE>
 struct GcPolicy {
   static constexpr bool kSplit = false;
+  static constexpr bool kWarpSpecialised = false;
+  static __host__ __device__ size_t ws_smem(int) { return 0; }
+  static __device__ __forceinline__ void cta_persistent(const GcApp&, const GraphView&, const Queue&, int,
+                                                        unsigned char*, LocalStats&) {}
   static __host__ __device__ size_t smem_bytes(int F) { return gc_cta_smem_bytes(F); }
   template <class Src, class Sink>
   static __device__ __forceinline__ void cta(const GcApp& app, const GraphView& g, const Src& src, const Sink& sink,
@@ -105,8 +116,8 @@ struct StageSrc {
 
 // dynamic shared memory per block for a worker kind
 template <class P>
-__host__ __device__ inline size_t worker_smem_bytes(int W, int F, int T) {
-  if (W == W_CTA) return P::smem_bytes(F);
+__host__ __device__ inline size_t worker_smem_bytes(int W, int F, int T, bool persistent = false) {
+  if (W == W_CTA) return (persistent && P::kWarpSpecialised) ? P::ws_smem(F) : P::smem_bytes(F);
   if (W == W_WARP) return (size_t)(T / 32) * (size_t)F * 4;
   return (size_t)T * (size_t)F * 4;
 }
@@ -119,7 +130,9 @@ __global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Qu
   q_arm(q);
   LocalStats st;
   RingSink sink{q};
-  if (W == W_CTA) {
+  if (W == W_CTA && P::kWarpSpecialised) {
+    P::cta_persistent(app, g, q, F, smem, st);
+  } else if (W == W_CTA) {
     __shared__ uint64_t s_first;
     __shared__ uint32_t s_n;
     for (;;) {
