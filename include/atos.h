@@ -74,7 +74,21 @@ typedef struct {
   int64_t queue_capacity; /* ring slots; 0 = auto (power of two >= 2n); rounded up to pow2     */
   double timeout_s;       /* device watchdog deadline in seconds; 0 = none                    */
   void* stream;           /* cudaStream_t to run on; NULL = legacy default stream             */
+  void* trace;            /* optional device buffer of atos_trace_rec (timeline);  */
+  int64_t trace_capacity; /*   records; one per processed batch; extra records are dropped    */
 } atos_config;
+
+/* One timeline record per batch processed by a persistent/discrete worker:
+ * %globaltimer at batch end, items in the batch, edges expanded, SM id.
+ * Sorted by t_ns they give cumulative work vs time (the paper's normalized
+ * throughput plots).  The number written is stats.trace_records. */
+typedef struct {
+  uint64_t t_ns;
+  uint32_t items;
+  uint32_t edges;
+  uint32_t sm;
+  uint32_t kind; /* 0 = BFS, 1 = PageRank, 2 = colouring */
+} atos_trace_rec;
 
 /* Per-call statistics (P:818 overwork, P:908 normalized throughput). */
 typedef struct {
@@ -92,6 +106,7 @@ typedef struct {
   int32_t _pad;
   double max_residue;       /* atos_pagerank: max residue at return (must be <= eps)      */
   int64_t chunk_tasks;      /* hub edge-chunk tasks processed (persistent CTA workers)    */
+  int64_t trace_records;    /* timeline records produced (may exceed trace_capacity)       */
 } atos_stats;
 
 /* Fill *cfg with defaults: persistent, CTA worker, 256 threads, fetch 256,

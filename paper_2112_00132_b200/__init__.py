@@ -52,7 +52,7 @@ class CConfig(ctypes.Structure):
                 ("bfs_filter", ctypes.c_int32), ("pr_activation", ctypes.c_int32), ("check_size", ctypes.c_int32),
                 ("gc_literal", ctypes.c_int32), ("pr_residue_fp64", ctypes.c_int32),
                 ("queue_capacity", ctypes.c_int64), ("timeout_s", ctypes.c_double),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64)]
 
 
 class CStats(ctypes.Structure):
@@ -60,7 +60,8 @@ class CStats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("tasks_popped", ctypes.c_int64),
                 ("tasks_pushed", ctypes.c_int64), ("edges_processed", ctypes.c_int64), ("rounds", ctypes.c_int64),
                 ("queue_high_water", ctypes.c_int64), ("bytes_sent", ctypes.c_int64), ("num_colors", ctypes.c_int32),
-                ("_pad", ctypes.c_int32), ("max_residue", ctypes.c_double), ("chunk_tasks", ctypes.c_int64)]
+                ("_pad", ctypes.c_int32), ("max_residue", ctypes.c_double), ("chunk_tasks", ctypes.c_int64),
+                ("trace_records", ctypes.c_int64)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k not in ("struct_size", "_pad")}
@@ -128,6 +129,7 @@ class Config:
     queue_capacity: int = 0
     timeout_s: float = 60.0
     stream: int | None = None      # raw cudaStream_t; None = torch current stream
+    trace: object = None           # Trace() buffer for the timeline, or None
 
     def to_c(self) -> CConfig:
         c = CConfig()
@@ -150,6 +152,9 @@ class Config:
             if torch.cuda.is_available():
                 s = torch.cuda.current_stream().cuda_stream
         c.stream = s or None
+        if self.trace is not None:
+            c.trace = self.trace.buf.data_ptr()
+            c.trace_capacity = self.trace.capacity
         return c
 
 
@@ -158,6 +163,26 @@ def _cfg(cfg: Config | None, kw) -> CConfig:
     if kw:
         cfg = Config(**{**cfg.__dict__, **kw})
     return cfg.to_c()
+
+
+class Trace:
+    """Device timeline buffer (atos_trace_rec records, one per processed batch).
+
+    After a call with ``Config(trace=tr)``: ``tr.records(stats)`` returns a
+    numpy structured array (t_ns, items, edges, sm, kind) sorted by time — the
+    cumulative-work-vs-time view of the paper's Figs. 4-6."""
+    DTYPE = np.dtype([("t_ns", "<u8"), ("items", "<u4"), ("edges", "<u4"), ("sm", "<u4"), ("kind", "<u4")])
+
+    def __init__(self, capacity: int = 1 << 20):
+        import torch
+        self.capacity = int(capacity)
+        self.buf = torch.zeros(self.capacity * 24, dtype=torch.uint8, device="cuda")
+
+    def records(self, stats: dict):
+        k = min(int(stats.get("trace_records", 0)), self.capacity)
+        raw = self.buf[: k * 24].cpu().numpy()
+        r = raw.view(self.DTYPE)
+        return np.sort(r, order="t_ns")
 
 
 # ---- graph -----------------------------------------------------------------
@@ -263,4 +288,4 @@ def color(g: Graph, cfg: Config | None = None, device: bool = False, out=None, *
     return col, k.value, st.to_dict()
 
 
-__all__ = ["Graph", "Config", "bfs", "pagerank", "color", "AtosError", "lib", "version", "UNREACHED", "EXPORTS"]
+__all__ = ["Graph", "Config", "Trace", "bfs", "pagerank", "color", "AtosError", "lib", "version", "UNREACHED", "EXPORTS"]

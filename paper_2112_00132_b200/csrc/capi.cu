@@ -97,6 +97,7 @@ static atos_status check_config(const atos_config* c) {
   if (!(c->timeout_s >= 0)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "timeout_s < 0");
   if (c->pr_activation != 0 && c->pr_activation != 1)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "pr_activation must be 0 or 1");
+  if (c->trace && c->trace_capacity < 0) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "trace_capacity < 0");
   if (c->pr_activation == 1 && c->check_size < 1)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "check_size < 1");
   return ATOS_OK;
@@ -279,7 +280,7 @@ atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, ui
   return ATOS_OK;
 }
 
-static Queue make_queue(atos_graph g, const atos_config& cfg) {
+static Queue make_queue(atos_graph g, const atos_config& cfg, uint32_t kind) {
   Queue q{};
   q.ring = g->ws.ring;
   q.mask = g->ws.cap - 1;
@@ -289,6 +290,9 @@ static Queue make_queue(atos_graph g, const atos_config& cfg) {
   q.deadline = 0;
   q.timeout_ns = cfg.timeout_s > 0 ? (uint64_t)(cfg.timeout_s * 1e9) : 0;
   q.head_floor = 0;
+  q.trace_kind = kind;
+  q.trace = reinterpret_cast<TraceRec*>(cfg.trace);
+  q.trace_cap = cfg.trace ? (uint64_t)cfg.trace_capacity : 0;
   return q;
 }
 
@@ -484,6 +488,7 @@ static atos_status finish_stats(LaunchCtx& c, atos_stats* st, bool bsp) {
     st->kernel_ms = kms;
     st->kernel_launches = c.launches + c.post_launches;
     st->chunk_tasks = (int64_t)w.h_ctl->chunk_done.v;
+    st->trace_records = (int64_t)w.h_ctl->trace_count.v;
     st->tasks_popped = (int64_t)w.h_ctl->stats[0].v - st->chunk_tasks;
     st->tasks_pushed = (int64_t)w.h_ctl->stats[1].v;
     st->edges_processed = (int64_t)w.h_ctl->stats[2].v;
@@ -544,9 +549,9 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
   BfsApp app{w.u32a, w.u32b, c.cfg.bfs_filter};
   using P = EdgeMapPolicy<BfsApp>;
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
-    CKS(run_persistent<P>(c, app, make_queue(g, c.cfg)));
+    CKS(run_persistent<P>(c, app, make_queue(g, c.cfg, 0)));
   } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
-    CKS(run_discrete<P>(c, app, make_queue(g, c.cfg), 1));
+    CKS(run_discrete<P>(c, app, make_queue(g, c.cfg, 0), 1));
   } else {
     // Alg. 1: double-buffered frontiers
     uint32_t h_src = (uint32_t)src;
@@ -591,9 +596,9 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
   CK(cudaEventRecord(w.ev[1], c.s));
   PrAppT<R> app{rank, res, (R)alpha, (R)eps};
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
-    CKS(run_persistent<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg)));
+    CKS(run_persistent<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1)));
   } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
-    CKS(run_discrete<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg), (uint64_t)n));
+    CKS(run_discrete<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1), (uint64_t)n));
   } else {
     // Alg. 3: push kernel over the frontier, then filter kernel over all vertices
     PrBspAppT<R> bapp{app};
@@ -701,9 +706,9 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
   CK(cudaEventRecord(w.ev[1], c.s));
   GcApp app{color, pend};
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
-    CKS(run_persistent<GcPolicy<GC_UBER>>(c, app, make_queue(g, c.cfg)));
+    CKS(run_persistent<GcPolicy<GC_UBER>>(c, app, make_queue(g, c.cfg, 2)));
   } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
-    CKS(run_discrete<GcPolicy<GC_UBER>>(c, app, make_queue(g, c.cfg), (uint64_t)n));
+    CKS(run_discrete<GcPolicy<GC_UBER>>(c, app, make_queue(g, c.cfg, 2), (uint64_t)n));
   } else {
     // Alg. 5: assign kernel then conflict-detect kernel over the frontier
     uint64_t cnt = (uint64_t)n;

@@ -126,6 +126,7 @@ __device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queu
       if (tid == 32) {
         st.popped += n;
         q_done(q, n);
+        q_trace(q, n, (uint64_t)total);
       }
       bar_arrive_n(3 + b, T);  // release buffer b
       b ^= 1;

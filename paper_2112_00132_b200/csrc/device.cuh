@@ -152,6 +152,7 @@ struct QueueCtl {
   Line64 high_water;    // max observed tail - head
   Line64 chunk_tail;    // hub chunk table: entries allocated
   Line64 chunk_done;    // hub chunk table: entries consumed
+  Line64 trace_count;   // timeline records produced
   Line64 stats[4];      // popped, pushed, edges, spare
   Line64 aux[4];        // app-specific counters (e.g. PR check cursor, colours)
 };
@@ -167,7 +168,35 @@ struct Queue {
   uint64_t head_floor;  // discrete rounds: every position < head_floor is claimed
   struct Chunk* chunks; // hub chunk table (persistent CTA edge-map workers); nullptr = no splitting
   uint64_t chunk_mask;  // table capacity - 1
+  struct TraceRec* trace;  // optional timeline (atos_trace_rec); nullptr = off
+  uint64_t trace_cap;
+  uint32_t trace_kind;
 };
+
+// Timeline record (layout == atos_trace_rec in include/atos.h).
+struct TraceRec {
+  uint64_t t_ns;
+  uint32_t items, edges, sm, kind;
+};
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+// One record per processed batch (single thread).
+__device__ __forceinline__ void q_trace(const Queue& q, uint32_t items, uint64_t edges) {
+  if (!q.trace) return;
+  const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->trace_count.v), 1ull);
+  if (i < q.trace_cap) {
+    TraceRec r;
+    r.t_ns = globaltimer_ns();
+    r.items = items;
+    r.edges = (uint32_t)(edges > 0xFFFFFFFFull ? 0xFFFFFFFFull : edges);
+    r.sm = smid();
+    r.kind = q.trace_kind;
+    q.trace[i] = r;
+  }
+}
 
 // A slice [e0, e1) of a hub's adjacency list, queued as its own task
 // (item = CHUNK_BIT | table index).  payload = the app payload computed when

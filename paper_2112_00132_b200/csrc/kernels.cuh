@@ -147,10 +147,12 @@ __global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Qu
       const uint64_t first = s_first;
       if (n == 0) break;
       RingSrc src{q, first};
+      const uint64_t e_before = st.edges;
       P::cta(app, g, src, sink, n, smem, F, st);  // ends with __syncthreads
       if (threadIdx.x == 0) {
         st.popped += n;
         q_done(q, n);
+        q_trace(q, n, st.edges - e_before);
       }
     }
   } else {
@@ -169,12 +171,16 @@ __global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Qu
       if (n == 0) break;
       stage_items(q, first, n, stage);
       StageSrc src{stage};
+      const uint64_t e_before = st.edges;
       if (W == W_WARP) P::warp(app, g, src, sink, n, st);
       else P::thread(app, g, src, sink, n, st);
       __syncwarp();
+      uint64_t de = st.edges - e_before;
+      if (W == W_THREAD) de = __reduce_add_sync(FULL_MASK, (unsigned)min(de, (uint64_t)0xFFFFFFFFu));
       if (lane_id() == 0) {
         st.popped += n;
         q_done(q, n);
+        q_trace(q, n, de);
       }
     }
   }
