@@ -77,6 +77,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->check_size = 32;
   c->gc_literal = 0;
   c->pr_residue_fp64 = 0;
+  c->adaptive_fetch = 1;
   c->queue_capacity = 0;
   c->timeout_s = 0.0;
   c->stream = nullptr;
@@ -362,6 +363,7 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
   if (per_sm < 1) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "kernel cannot be resident with %d threads", T);
   int blocks = per_sm * c.g->sms;
   if (c.cfg.num_blocks > 0) blocks = std::min(blocks, c.cfg.num_blocks);  // persistent: <= resident maximum
+  if (c.cfg.adaptive_fetch) qq.workers = (uint32_t)(W == W_CTA ? blocks : blocks * (T / 32));
   kern<<<blocks, T, smem, c.s>>>(app, c.gv, qq, F);
   CK(cudaGetLastError());
   c.launches++;

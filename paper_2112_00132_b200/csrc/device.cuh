@@ -171,6 +171,7 @@ struct Queue {
   struct TraceRec* trace;  // optional timeline (atos_trace_rec); nullptr = off
   uint64_t trace_cap;
   uint32_t trace_kind;
+  uint32_t workers;  // adaptive fetch: number of concurrent poppers (0 = off)
 };
 
 // Timeline record (layout == atos_trace_rec in include/atos.h).
@@ -364,7 +365,17 @@ __device__ __forceinline__ void q_thread_push(const Queue& q, uint32_t k, F item
 // Returns the count claimed (0 if nothing is published right now).
 __device__ __forceinline__ uint32_t q_try_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& qlen) {
   long long* cnt = reinterpret_cast<long long*>(&q.ctl->count.v);
-  if ((long long)ld_relaxed_u64(&q.ctl->count.v) <= 0) return 0;
+  const long long seen = (long long)ld_relaxed_u64(&q.ctl->count.v);
+  if (seen <= 0) return 0;
+  // Adaptive fetch: while the queue is short, take only a fair share
+  // ceil(count / workers) (>= 1) so a small frontier — e.g. the ~200 chunk
+  // tasks of the source hub — spreads over all workers instead of landing in
+  // one FETCH-sized batch (measured: 28 batches on 24 SMs in the first 0.7 ms
+  // of RMAT-24 BFS).  FETCH_SIZE stays the upper bound.
+  if (q.workers) {
+    const long long share = (seen + q.workers - 1) / q.workers;
+    if (share < (long long)want) want = (uint32_t)share;
+  }
   const long long old = atomicAdd(reinterpret_cast<unsigned long long*>(cnt), (unsigned long long)(-(long long)want));
   uint32_t n;
   if (old >= (long long)want) {

@@ -55,12 +55,27 @@ struct BfsApp {
   // improvements is expanded at most once per distinct depth it is popped at.
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
-    e0 = ld_nc_s64(g.off + v);
-    e1 = ld_nc_s64(g.off + v + 1);
-    const uint32_t d = ld_relaxed_u32(dist + v);
-    p = d + 1u;
-    if (e1 == e0) return false;
-    return atomicMin(done + v, d) > d;
+    Pre x = begin_load(v, g);
+    e0 = x.e0;
+    e1 = x.e1;
+    return begin_commit(v, x, p);
+  }
+  // begin() in two phases so a queue agent can overlap many items' loads.
+  struct Pre {
+    int64_t e0, e1;
+    uint32_t d;
+  };
+  __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
+    Pre x;
+    x.e0 = ld_nc_s64(g.off + v);
+    x.e1 = ld_nc_s64(g.off + v + 1);
+    x.d = ld_relaxed_u32_nc(dist + v);
+    return x;
+  }
+  __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
+    p = x.d + 1u;
+    if (x.e1 == x.e0) return false;
+    return atomicMin(done + v, x.d) > x.d;
   }
   __device__ __forceinline__ bool edge(Payload nd, uint32_t w) const {
     if (filter && nd >= ld_relaxed_u32(dist + w)) return false;
@@ -91,13 +106,28 @@ struct PrAppT {
   using Payload = R;
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
-    e0 = ld_nc_s64(g.off + v);
-    e1 = ld_nc_s64(g.off + v + 1);
-    const R r = atomic_take(res + v);
-    if (r == R(0)) return false;
-    atomicAdd(rank + v, (double)r);
-    if (e1 == e0) return false;
-    p = alpha * r / (R)(e1 - e0);
+    Pre x = begin_load(v, g);
+    e0 = x.e0;
+    e1 = x.e1;
+    return begin_commit(v, x, p);
+  }
+  struct Pre {
+    int64_t e0, e1;
+    R r;
+  };
+  // the residue exchange is issued in the load phase (its result is only used in commit)
+  __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
+    Pre x;
+    x.e0 = ld_nc_s64(g.off + v);
+    x.e1 = ld_nc_s64(g.off + v + 1);
+    x.r = atomic_take(res + v);
+    return x;
+  }
+  __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
+    if (x.r == R(0)) return false;
+    atomicAdd(rank + v, (double)x.r);
+    if (x.e1 == x.e0) return false;
+    p = alpha * x.r / (R)(x.e1 - x.e0);
     return true;
   }
   __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
@@ -345,6 +375,30 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
   return pushed;
 }
 
+// Publish edges [e0 + CHUNK_EDGES, e1) of hub `v` as chunk tasks; returns the
+// new end of the range the caller keeps (its first chunk).
+template <class Payload>
+__device__ __noinline__ int64_t split_hub(const Queue* cq, uint32_t v, int64_t e0, int64_t e1, Payload p) {
+  const uint32_t k = (uint32_t)((e1 - e0 - 1) / CHUNK_EDGES);  // chunks beyond the first
+  const unsigned long long base =
+      atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_tail.v), (unsigned long long)k);
+  if (base + k - ld_relaxed_u64(&cq->ctl->chunk_done.v) > cq->chunk_mask + 1) {
+    q_raise(*cq, ABORT_OVERFLOW);
+    return e1;
+  }
+  const uint64_t pb = pack_payload(p);
+  for (uint32_t j = 0; j < k; ++j) {
+    Chunk* c = cq->chunks + ((base + j) & cq->chunk_mask);
+    c->payload = pb;
+    c->v = v;
+    c->e0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
+    c->e1 = min(e1, e0 + CHUNK_EDGES * (int64_t)(j + 2));
+  }
+  __threadfence();  // chunk entries visible before their tasks
+  q_thread_push(*cq, k, [&](uint32_t j) { return CHUNK_BIT | (uint32_t)((base + j) & cq->chunk_mask); });
+  return e0 + CHUNK_EDGES;
+}
+
 // Turn a popped queue item into an edge range + payload (a4 -> a5):
 // a chunk task reads its table entry; a vertex runs the app's begin() and, if
 // it is a hub and splitting is on (cq != nullptr), publishes all but its first
@@ -363,26 +417,7 @@ __device__ __forceinline__ bool prepare_item(const App& app, const GraphView& g,
     return ok;
   }
   if (!app.begin(item, g, e0, e1, p)) return false;
-  if (cq && e1 - e0 > SPLIT_DEG) {
-    const uint32_t k = (uint32_t)((e1 - e0 - 1) / CHUNK_EDGES);  // chunks beyond the first
-    const unsigned long long base =
-        atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_tail.v), (unsigned long long)k);
-    if (base + k - ld_relaxed_u64(&cq->ctl->chunk_done.v) > cq->chunk_mask + 1) {
-      q_raise(*cq, ABORT_OVERFLOW);
-      return false;
-    }
-    const uint64_t pb = pack_payload(p);
-    for (uint32_t j = 0; j < k; ++j) {
-      Chunk* c = cq->chunks + ((base + j) & cq->chunk_mask);
-      c->payload = pb;
-      c->v = item;
-      c->e0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
-      c->e1 = min(e1, e0 + CHUNK_EDGES * (int64_t)(j + 2));
-    }
-    __threadfence();  // chunk entries visible before their tasks
-    q_thread_push(*cq, k, [&](uint32_t j) { return CHUNK_BIT | (uint32_t)((base + j) & cq->chunk_mask); });
-    e1 = e0 + CHUNK_EDGES;
-  }
+  if (cq && e1 - e0 > SPLIT_DEG) e1 = split_hub(cq, item, e0, e1, p);
   return true;
 }
 
