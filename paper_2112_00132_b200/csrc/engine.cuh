@@ -45,10 +45,10 @@ struct BfsApp {
   // any atomic (memory-level parallelism).  The probe may hit a stale L1 copy
   // (>= the current value): it only lets through atomics that turn out not to
   // improve, never suppresses one that would.
-  __device__ __forceinline__ Probe probe(uint32_t w) const { return filter ? ld_relaxed_cta_u32(dist + w) : 0xFFFFFFFFu; }
+  __device__ __forceinline__ Probe probe(uint32_t w) const { return filter ? ld_probe_hot(dist + w) : 0xFFFFFFFFu; }
   __device__ __forceinline__ bool commit(Payload nd, uint32_t w, Probe pr) const {
     if (nd >= pr) return false;
-    return nd < atomicMin(dist + w, nd);
+    return nd < atom_min_hot(dist + w, nd);
   }
   // Expand v at its CURRENT depth d (R3) unless some task already expanded
   // (or is expanding) v at depth <= d: a vertex pushed k times by k
@@ -69,7 +69,7 @@ struct BfsApp {
     Pre x;
     x.e0 = ld_nc_s64(g.off + v);
     x.e1 = ld_nc_s64(g.off + v + 1);
-    x.d = ld_relaxed_u32_nc(dist + v);
+    x.d = ld_relaxed_hot(dist + v);
     return x;
   }
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
@@ -79,7 +79,7 @@ struct BfsApp {
   }
   __device__ __forceinline__ bool edge(Payload nd, uint32_t w) const {
     if (filter && nd >= ld_relaxed_u32(dist + w)) return false;
-    return nd < atomicMin(dist + w, nd);
+    return nd < atom_min_hot(dist + w, nd);
   }
 };
 
@@ -131,7 +131,7 @@ struct PrAppT {
     return true;
   }
   __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
-    const R old = atomicAdd(res + w, c);
+    const R old = atom_add_hot(res + w, c);
     return old <= eps && add_rn(old, c) > eps;
   }
   using Probe = int;
