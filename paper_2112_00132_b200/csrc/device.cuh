@@ -138,17 +138,17 @@ __device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
 // hot per-vertex state: relaxed gpu-scope atomics / loads with L2 evict_last
 __device__ __forceinline__ uint32_t atom_min_hot(uint32_t* p, uint32_t v) {
   uint32_t o;
-  asm volatile("atom.relaxed.gpu.global.min.L2::cache_hint.u32 %0, [%1], %2, %3;" : "=r"(o) : "l"(p), "r"(v), "l"(pol_evict_last()) : "memory");
+  asm volatile("atom.relaxed.gpu.global.min.L2::cache_hint.u32 %0, [%1], %2, %3;" : "=r"(o) : "l"(p), "r"(v), "l"(pol_evict_last()));
   return o;
 }
 __device__ __forceinline__ float atom_add_hot(float* p, float v) {
   float o;
-  asm volatile("atom.relaxed.gpu.global.add.L2::cache_hint.f32 %0, [%1], %2, %3;" : "=f"(o) : "l"(p), "f"(v), "l"(pol_evict_last()) : "memory");
+  asm volatile("atom.relaxed.gpu.global.add.L2::cache_hint.f32 %0, [%1], %2, %3;" : "=f"(o) : "l"(p), "f"(v), "l"(pol_evict_last()));
   return o;
 }
 __device__ __forceinline__ double atom_add_hot(double* p, double v) {
   double o;
-  asm volatile("atom.relaxed.gpu.global.add.L2::cache_hint.f64 %0, [%1], %2, %3;" : "=d"(o) : "l"(p), "d"(v), "l"(pol_evict_last()) : "memory");
+  asm volatile("atom.relaxed.gpu.global.add.L2::cache_hint.f64 %0, [%1], %2, %3;" : "=d"(o) : "l"(p), "d"(v), "l"(pol_evict_last()));
   return o;
 }
 __device__ __forceinline__ uint32_t ld_probe_hot(const uint32_t* p) {  // cta scope: may hit a stale L1 copy

@@ -47,9 +47,15 @@ struct BfsApp {
   // improve, never suppresses one that would.
   __device__ __forceinline__ Probe probe(uint32_t w) const { return filter ? ld_probe_hot(dist + w) : 0xFFFFFFFFu; }
   __device__ __forceinline__ bool commit(Payload nd, uint32_t w, Probe pr) const {
-    if (nd >= pr) return false;
-    return nd < atom_min_hot(dist + w, nd);
+    return decide(nd, w, pr, issue(nd, w, pr));
   }
+  // commit split into issue (the atomic) and decide (uses its result), so a
+  // thread's UNROLL atomics are all in flight before any result is consumed.
+  using Raw = uint32_t;
+  __device__ __forceinline__ Raw issue(Payload nd, uint32_t w, Probe pr) const {
+    return nd < pr ? atom_min_hot(dist + w, nd) : 0u;
+  }
+  __device__ __forceinline__ bool decide(Payload nd, uint32_t, Probe pr, Raw old) const { return nd < pr && nd < old; }
   // Expand v at its CURRENT depth d (R3) unless some task already expanded
   // (or is expanding) v at depth <= d: a vertex pushed k times by k
   // improvements is expanded at most once per distinct depth it is popped at.
@@ -138,6 +144,11 @@ struct PrAppT {
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
   __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
+  using Raw = R;
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { return atom_add_hot(res + w, c); }
+  __device__ __forceinline__ bool decide(Payload c, uint32_t, Probe, Raw old) const {
+    return old <= eps && add_rn(old, c) > eps;
+  }
 };
 
 // BSP PageRank push kernel body (Alg. 3 lines 11-16): same push
@@ -158,6 +169,9 @@ struct PrBspAppT {
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
   __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
+  using Raw = int;
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { edge(c, w); return 0; }
+  __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
 };
 
 // ------------------------------------------------------- sources / sinks ---
@@ -367,9 +381,16 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k)
       if (idx[k] >= 0) pr[k] = app.probe(w[k]);
+    typename App::Raw raw[LBS_UNROLL];
+    typename App::Payload pk[LBS_UNROLL];
+#pragma unroll
+    for (int k = 0; k < LBS_UNROLL; ++k) {
+      pk[k] = idx[k] >= 0 ? pay[idx[k]] : typename App::Payload{};
+      if (idx[k] >= 0) raw[k] = app.issue(pk[k], w[k], pr[k]);
+    }
     bool act[LBS_UNROLL];
 #pragma unroll
-    for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.commit(pay[idx[k]], w[k], pr[k]);
+    for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.decide(pk[k], w[k], pr[k], raw[k]);
     pushed += sink.template warp_push_multi<LBS_UNROLL>(act, w);
   }
   return pushed;
@@ -478,9 +499,13 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if (v) pr[k] = app.probe(w[k]);
+    typename App::Raw raw[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v) raw[k] = app.issue(p, w[k], pr[k]);
     bool act[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) act[k] = v && app.commit(p, w[k], pr[k]);
+    for (int k = 0; k < 4; ++k) act[k] = v && app.decide(p, w[k], pr[k], raw[k]);
     pushed += sink.template warp_push_multi<4>(act, w);
   }
   {

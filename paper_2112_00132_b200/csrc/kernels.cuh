@@ -336,7 +336,11 @@ struct PrInitAppT {
   }
   using Probe = int;
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
-  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
+  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
+  using Raw = int;
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { atomicAdd(res + w, c); return 0; }
+  __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
 };
 
 __global__ void k_f64_to_f32(const double* a, float* b, int64_t n) {
