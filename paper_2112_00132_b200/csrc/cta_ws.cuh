@@ -16,6 +16,8 @@
 // every claimed slot before it pushes anything (split chunks), so it never
 // waits on a wrapped slot it holds itself.
 #pragma once
+#include <type_traits>
+
 #include "engine.cuh"
 
 namespace atos {
@@ -27,9 +29,14 @@ template <class Payload>
 __host__ __device__ constexpr size_t ws_buf_bytes(int F) {
   return (size_t)F * 8 + ((size_t)F + 1) * 8 + (((size_t)F * sizeof(Payload) + 15) & ~(size_t)15);
 }
+constexpr uint32_t COMB_SLOTS = 2048;  // push-combiner table (2x the hot set)
 template <class Payload>
-__host__ __device__ constexpr size_t ws_smem_bytes(int F) {
-  return 2 * ws_buf_bytes<Payload>(F) + 64;
+__host__ __device__ constexpr size_t comb_bytes() {
+  return (size_t)COMB_SLOTS * (4 + sizeof(Payload) + 4) + 16;
+}
+template <class Payload>
+__host__ __device__ constexpr size_t ws_smem_bytes(int F, bool comb) {
+  return 2 * ws_buf_bytes<Payload>(F) + 64 + (comb ? comb_bytes<Payload>() : 0);
 }
 
 // Warp-cooperative exclusive scan of a[0..n) into a[0..n], a[n] = total.
@@ -171,15 +178,53 @@ __device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queu
     int b = 0;
     uint32_t pushed = 0;
     uint64_t edges = 0;
+    // PageRank: shared-memory combiner for hot destinations
+    using Comb = typename std::conditional<App::kCombine, SmemComb<Payload>, NoComb>::type;
+    Comb comb{};
+    if constexpr (App::kCombine) {
+      unsigned char* cb = smem + 2 * bb + 64;
+      comb.key = reinterpret_cast<uint32_t*>(cb);
+      comb.val = reinterpret_cast<Payload*>(cb + COMB_SLOTS * 4);
+      comb.used = reinterpret_cast<uint32_t*>(cb + COMB_SLOTS * (4 + sizeof(Payload)));
+      comb.nused = comb.used + COMB_SLOTS;
+      comb.mask = COMB_SLOTS - 1;
+      for (uint32_t i = tid - 32; i < COMB_SLOTS; i += T - 32) {
+        comb.key[i] = SmemComb<Payload>::EMPTY;
+        comb.val[i] = Payload(0);
+      }
+      if (tid == 32) *comb.nused = 0;
+      bar_sync_n(5, T - 32);
+    }
     for (;;) {
       bar_sync_n(1 + b, T);
       const uint32_t n = hdr[b];
       if (n == 0) break;
       const int64_t* pre = buf_pre(b);
       const int64_t total = pre[n];
-      pushed += lbs_expand(app, g, sink, pre, buf_e0(b), buf_pay(b), (int)n, total, wid - 1, nw);
+      pushed += lbs_expand(app, g, sink, pre, buf_e0(b), buf_pay(b), (int)n, total, wid - 1, nw, comb);
       edges += total;
       bar_sync_n(5, T - 32);  // every worker's pushes for this batch are reserved
+      if constexpr (App::kCombine) {
+        // flush: one global atomic per combined destination; push on a crossing
+        const uint32_t nu = *comb.nused;
+        for (uint32_t ib = (uint32_t)(wid - 1) * 32; ib < nu; ib += (uint32_t)nw * 32) {
+          const uint32_t i = ib + lane;
+          bool act[1] = {false};
+          uint32_t item[1] = {0};
+          if (i < nu) {
+            const uint32_t h = comb.used[i];
+            const uint32_t w = comb.key[h];
+            const Payload c = comb.val[h];
+            comb.key[h] = SmemComb<Payload>::EMPTY;
+            comb.val[h] = Payload(0);
+            act[0] = app.decide(c, w, 0, app.issue(c, w, 0));
+            item[0] = w;
+          }
+          pushed += sink.template warp_push_multi<1>(act, item);
+        }
+        bar_sync_n(5, T - 32);
+        if (tid == 32) *comb.nused = 0;
+      }
       if (tid == 32) {
         st.popped += n;
         q_done(q, n);

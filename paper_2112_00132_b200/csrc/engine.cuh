@@ -33,6 +33,7 @@ struct GraphView {
 // per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
 // (strict, R2).
 struct BfsApp {
+  static constexpr bool kCombine = false;
   uint32_t* dist;
   uint32_t* done;  // done[v] = smallest depth at which v has been expanded (init MAX)
   int filter;
@@ -106,6 +107,7 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 
 template <class R>
 struct PrAppT {
+  static constexpr bool kCombine = true;
   double* rank;
   R* res;
   R alpha, eps;
@@ -155,6 +157,7 @@ struct PrAppT {
 // but the frontier is rebuilt by the filter kernel, so nothing is appended.
 template <class R>
 struct PrBspAppT {
+  static constexpr bool kCombine = false;
   PrAppT<R> base;
   using Payload = R;
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
@@ -349,10 +352,49 @@ __device__ __forceinline__ const Queue* chunk_queue(const RingSrc& s) { return s
 // lane locates its edges' items by binary search bounded by the owners of the
 // warp's first and last edge, loads UNROLL columns, issues UNROLL probes, then
 // UNROLL commits, then ONE aggregated push.  Returns the pushes (per lane 0).
-template <class App, class Sink>
+// No push combining (BFS, and every non-warp-specialised path).
+struct NoComb {
+  static constexpr bool kOn = false;
+  template <class P>
+  __device__ __forceinline__ bool add(uint32_t, P) const { return false; }
+};
+
+// Shared-memory push combiner for PageRank: contributions to HOT_BIT-marked
+// destinations (the graph's highest in-degree vertices) are summed in a
+// direct-mapped table and applied with ONE global atomic per destination per
+// batch (at flush), instead of one per edge.  Same-address atomics serialise
+// in L2: on RMAT the top vertex alone receives ~0.2% of all PR pushes.  An add
+// is a delayed, merged residue update, so threshold-crossing activation (R6)
+// is unchanged: the flush's atomic sees the old residue and pushes on a crossing.
+template <class R>
+struct SmemComb {
+  static constexpr bool kOn = true;
+  static constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+  uint32_t* key;
+  R* val;
+  uint32_t* used;
+  uint32_t* nused;
+  uint32_t mask;  // table size - 1
+  __device__ __forceinline__ bool add(uint32_t w, R c) const {
+    const uint32_t h = (w * 0x9E3779B1u) >> 7 & mask;
+    uint32_t k = key[h];
+    if (k == EMPTY) {
+      k = atomicCAS(key + h, EMPTY, w);
+      if (k == EMPTY) {
+        k = w;
+        used[atomicAdd(nused, 1u)] = h;
+      }
+    }
+    if (k != w) return false;  // collision with another hot vertex: global path
+    atomicAdd(val + h, c);
+    return true;
+  }
+};
+
+template <class App, class Sink, class Comb = NoComb>
 __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
                                                const int64_t* e0s, const typename App::Payload* pay, int n,
-                                               int64_t total, int wi, int nw) {
+                                               int64_t total, int wi, int nw, const Comb& comb = Comb{}) {
   const int lane = lane_id();
   const int64_t stride = (int64_t)nw * 32 * LBS_UNROLL;
   uint32_t pushed = 0;
@@ -374,9 +416,16 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
       if (e < total) {
         lo = lbs_find_range(pre, lo, hi, e);
         idx[k] = lo;
-        w[k] = (uint32_t)ld_stream_s32(g.col + e0s[lo] + (e - pre[lo]));
+        w[k] = (uint32_t)ld_col_raw(g.col + e0s[lo] + (e - pre[lo]));
       }
     }
+    if (Comb::kOn) {
+#pragma unroll
+      for (int k = 0; k < LBS_UNROLL; ++k)
+        if (idx[k] >= 0 && (w[k] & HOT_BIT) && comb.add(w[k] & COL_MASK, pay[idx[k]])) idx[k] = -1;
+    }
+#pragma unroll
+    for (int k = 0; k < LBS_UNROLL; ++k) w[k] &= COL_MASK;
     typename App::Probe pr[LBS_UNROLL];
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k)

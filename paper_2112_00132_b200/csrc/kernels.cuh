@@ -23,7 +23,7 @@ struct EdgeMapPolicy {
   static constexpr bool kWarpSpecialised = true;
   using Payload = typename App::Payload;
   static __host__ __device__ size_t smem_bytes(int F) { return cta_smem_bytes<Payload>(F); }
-  static __host__ __device__ size_t ws_smem(int F) { return ws_smem_bytes<Payload>(F); }
+  static __host__ __device__ size_t ws_smem(int F) { return ws_smem_bytes<Payload>(F, App::kCombine); }
   static __device__ __forceinline__ void cta_persistent(const App& app, const GraphView& g, const Queue& q, int F,
                                                         unsigned char* smem, LocalStats& st) {
     cta_ws_persistent(app, g, q, F, smem, st);
@@ -320,6 +320,7 @@ __global__ void k_bfs_init(uint32_t* dist, uint32_t* done, int64_t n, int64_t sr
 // app that pushes c = (1-a) a / deg(v) to every out-neighbour, no activation.
 template <class R>
 struct PrInitAppT {
+  static constexpr bool kCombine = false;
   R* res;
   R c0;  // (1 - alpha) * alpha
   using Payload = R;
