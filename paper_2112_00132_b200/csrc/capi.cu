@@ -172,6 +172,20 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     CK(cudaMemcpy(g->d_off, off, (size_t)(n + 1) * sizeof(int64_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
     if (m) CK(cudaMemcpy(g->d_col, col, (size_t)m * sizeof(int32_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
   }
+  // L2 set-aside for evict_last (persisting) lines: the per-vertex state the
+  // edge loop hits at random (BFS dist, PR residue) is accessed with an
+  // evict_last policy, which only persists within this carve-out (default 0;
+  // measured 51% atomic misses on a 64 MB residue array without it).
+  {
+    int max_persist = 0;
+    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device) == cudaSuccess &&
+        max_persist > 0) {
+      size_t cur = 0;
+      if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < (size_t)max_persist)
+        (void)cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+      (void)cudaGetLastError();
+    }
+  }
   CK(cudaMalloc(&g->d_scratch, 256));
   CK(cudaMemset(g->d_scratch, 0, 256));
   if (flags & ATOS_GRAPH_VALIDATE) {

@@ -306,7 +306,9 @@ __device__ __forceinline__ bool q_store_slot(const Queue& q, uint64_t p, uint32_
   // atomic is performed at L2 — the point of coherence — before this store
   // issues.  A st.release here cost a MEMBAR+ERRBAR per push (19% of BFS
   // stall samples, profiles/r01_bfs_rmat24_v1).
-  st_relaxed_u64(slot, ((uint64_t)(2u * lap + 1u) << 32) | item);
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(slot),
+               "l"(((uint64_t)(2u * lap + 1u) << 32) | item), "l"(pol_evict_first())
+               : "memory");
   return true;
 }
 
