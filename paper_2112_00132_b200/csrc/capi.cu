@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdarg>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/atos.h"
@@ -347,6 +348,8 @@ static Queue make_queue(atos_graph g, const atos_config& cfg, uint32_t kind) {
   q.timeout_ns = cfg.timeout_s > 0 ? (uint64_t)(cfg.timeout_s * 1e9) : 0;
   q.head_floor = 0;
   q.trace_kind = kind;
+  q.backoff_ns = 256;
+  if (const char* e = getenv("ATOS_BACKOFF_NS")) q.backoff_ns = (uint32_t)atoi(e);  // tuning experiments only
   q.trace = reinterpret_cast<TraceRec*>(cfg.trace);
   q.trace_cap = cfg.trace ? (uint64_t)cfg.trace_capacity : 0;
   return q;

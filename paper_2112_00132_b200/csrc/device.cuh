@@ -225,6 +225,7 @@ struct Queue {
   uint64_t trace_cap;
   uint32_t trace_kind;
   uint32_t workers;  // adaptive fetch: number of concurrent poppers (0 = off)
+  uint32_t backoff_ns;  // idle-poll backoff cap
 };
 
 // Timeline record (layout == atos_trace_rec in include/atos.h).
@@ -466,7 +467,7 @@ __device__ __forceinline__ uint32_t q_pop_or_quit(const Queue& q, uint32_t want,
     if (p == t) return 0;
     if (q_aborted(q) || q_timed_out(q)) return 0;
     if (ns) __nanosleep(ns);
-    ns = ns == 0 ? 32 : (ns < 512 ? ns * 2 : ns);
+    ns = ns == 0 ? 32 : (ns < q.backoff_ns ? ns * 2 : ns);
   }
 }
 
