@@ -43,7 +43,6 @@ typedef enum {
 } atos_status;
 
 typedef struct atos_graph_s* atos_graph; /* opaque; owns (or borrows) a device CSR */
-typedef struct atos_comm_s* atos_comm;   /* opaque multi-GPU communicator (NCCL)   */
 
 /* Kernel strategy, P:318-325 ("persistent" vs "discrete"); BSP = Alg. 1/3/5. */
 typedef enum { ATOS_KERNEL_PERSISTENT = 0, ATOS_KERNEL_DISCRETE = 1, ATOS_KERNEL_BSP = 2 } atos_kernel;
@@ -156,23 +155,49 @@ const char* atos_last_error(void);
 const char* atos_version(void);
 
 /* ---------------- multi-GPU (one process per GPU, 1-D vertex partition) ---------------- */
-/* Rank r owns global vertices [v_begin, v_end) and their out-rows; columns are
- * global ids.  Remote activations are batched per round and exchanged with an
- * NCCL all-to-all over NVLink.  NCCL is loaded at run time. */
+/* BFS and PageRank shard by a 1-D vertex split (callers permute
+ * vertex ids first: a block split of RMAT is 3.4x edge-imbalanced).  Each rank
+ * runs the same persistent queue kernel on its own vertices to LOCAL
+ * quiescence; activations of remote vertices are batched per round into one
+ * message buffer grouped by destination rank; the caller exchanges the buffers
+ * with an all-to-all (torch.distributed -> NCCL over NVLink/NVSwitch) and
+ * applies what it received; the run ends when a round sends no message on any
+ * rank (an all-reduce).  A message is (uint64)(dest_local_id << 32 | payload),
+ * payload = BFS depth (u32) or PageRank residue contribution (f32 bits).
+ * BFS: a remote vertex is sent at most once per improvement (per-rank
+ * sent_min filter).  PageRank: remote contributions are accumulated per
+ * destination vertex and flushed every round (never thresholded, so no mass
+ * is stranded).  Colouring is single-GPU (replicas only). */
 
-/* Write a 128-byte NCCL unique id into id_out (call on rank 0, broadcast it). */
-atos_status atos_comm_unique_id(uint8_t id_out[128]);
-/* Create the communicator on the current CUDA device. */
-atos_status atos_comm_init(int32_t rank, int32_t world, const uint8_t id[128], atos_comm* out);
-atos_status atos_comm_destroy(atos_comm c);
-/* Partitioned graph: local_row_offsets int64[(v_end-v_begin)+1] (starting at 0),
- * col_global int32[local_m] global ids < global_n. */
-atos_status atos_graph_create_partitioned(atos_comm c, int64_t global_n, int64_t v_begin,
-                                          int64_t v_end, const int64_t* local_row_offsets,
-                                          const int32_t* col_global, int64_t local_m,
-                                          uint32_t flags, atos_graph* out);
-/* atos_bfs / atos_pagerank on a partitioned graph: src is a global id; outputs
- * cover the local range [v_begin, v_end) (v_end - v_begin entries). */
+/* Partitioned graph for rank `rank` of `world`: it owns global vertices
+ * [bounds[rank], bounds[rank+1]) (bounds: host int64[world+1], bounds[0] = 0,
+ * bounds[world] = global_n).  local_row_offsets int64[n_local+1] starting at 0,
+ * col_global int32[local_m] global ids.  Copies like atos_graph_create (flags:
+ * DEVICE_PTRS / VALIDATE honoured; BORROW ignored). */
+atos_status atos_graph_create_partitioned(int64_t global_n, int32_t world, int32_t rank,
+                                          const int64_t* bounds, const int64_t* local_row_offsets,
+                                          const int32_t* col_global, int64_t local_m, uint32_t flags,
+                                          atos_graph* out);
+/* Start a partitioned run: app 0 = BFS from global vertex src (alpha/eps
+ * ignored), app 1 = PageRank(alpha, eps) (src ignored).  Initialises local
+ * state (timed into the first round's stats). */
+atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, float alpha, float eps,
+                            const atos_config* cfg);
+/* Run the local persistent kernel to quiescence, then gather this round's
+ * outgoing messages.  send_counts: host int64[world] (messages per
+ * destination; [rank] is 0). */
+atos_status atos_part_run(atos_graph g, int64_t* send_counts);
+/* Copy the round's messages, grouped by destination rank in rank order, to
+ * dst (host or device, capacity cap messages; cap >= sum(send_counts)). */
+atos_status atos_part_pack(atos_graph g, uint64_t* dst, int64_t cap);
+/* Apply received messages (host or device buffer of `count` uint64):
+ * BFS atomicMin + push on improvement; PageRank atomicAdd + push on an
+ * eps crossing. */
+atos_status atos_part_apply(atos_graph g, const uint64_t* msgs, int64_t count);
+/* Finish: write the local results (BFS: uint32 depth, PageRank: float rank;
+ * n_local = bounds[rank+1]-bounds[rank] entries, host or device) and the
+ * accumulated statistics (rounds = exchange rounds; bytes_sent = message bytes). */
+atos_status atos_part_finish(atos_graph g, void* out, atos_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,8 @@ UNREACHED = 0xFFFFFFFF
 EXPORTS = [
     "atos_config_default", "atos_graph_create", "atos_graph_destroy", "atos_graph_info", "atos_bfs",
     "atos_pagerank", "atos_color", "atos_status_string", "atos_last_error", "atos_version",
-    "atos_comm_unique_id", "atos_comm_init", "atos_comm_destroy", "atos_graph_create_partitioned",
+    "atos_graph_create_partitioned", "atos_part_begin", "atos_part_run", "atos_part_pack", "atos_part_apply",
+    "atos_part_finish",
 ]
 
 
@@ -92,13 +93,15 @@ def lib():
         L.atos_status_string.restype = ctypes.c_char_p
         L.atos_last_error.restype = ctypes.c_char_p
         L.atos_version.restype = ctypes.c_char_p
-        L.atos_comm_unique_id.argtypes = [vp]
-        L.atos_comm_init.argtypes = [i32, i32, vp, ctypes.POINTER(vp)]
-        L.atos_comm_destroy.argtypes = [vp]
-        L.atos_graph_create_partitioned.argtypes = [vp, i64, i64, i64, vp, vp, i64, u32, ctypes.POINTER(vp)]
+        L.atos_graph_create_partitioned.argtypes = [i64, i32, i32, vp, vp, vp, i64, u32, ctypes.POINTER(vp)]
+        L.atos_part_begin.argtypes = [vp, i32, i64, ctypes.c_float, ctypes.c_float, cfgp]
+        L.atos_part_run.argtypes = [vp, vp]
+        L.atos_part_pack.argtypes = [vp, vp, i64]
+        L.atos_part_apply.argtypes = [vp, vp, i64]
+        L.atos_part_finish.argtypes = [vp, vp, stp]
         for f in ("atos_graph_create", "atos_graph_destroy", "atos_graph_info", "atos_bfs", "atos_pagerank",
-                  "atos_color", "atos_comm_unique_id", "atos_comm_init", "atos_comm_destroy",
-                  "atos_graph_create_partitioned"):
+                  "atos_color", "atos_graph_create_partitioned", "atos_part_begin", "atos_part_run",
+                  "atos_part_pack", "atos_part_apply", "atos_part_finish"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib

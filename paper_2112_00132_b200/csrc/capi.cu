@@ -11,6 +11,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "../../include/atos.h"
 #include "kernels.cuh"
@@ -106,12 +107,13 @@ static atos_status check_config(const atos_config* c) {
 }
 
 // ------------------------------------------------------------------ graph
-__global__ void k_validate(const int64_t* off, const int32_t* col, int64_t n, int64_t m, unsigned int* bad) {
+__global__ void k_validate(const int64_t* off, const int32_t* col, int64_t n, int64_t m, int64_t col_bound,
+                           unsigned int* bad) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = tid; v < n; v += stride)
     if (off[v + 1] < off[v]) atomicOr(bad, 1u);
   for (int64_t e = tid; e < m; e += stride)
-    if (col[e] < 0 || (int64_t)col[e] >= n) atomicOr(bad, 2u);
+    if (col[e] < 0 || (int64_t)col[e] >= col_bound) atomicOr(bad, 2u);
   if (tid == 0 && (off[0] != 0 || off[n] != m)) atomicOr(bad, 4u);
 }
 __global__ void k_max_degree(const int64_t* off, int64_t n, unsigned long long* out) {
@@ -154,7 +156,8 @@ static atos_status device_sms(int* sms) {
 }
 
 atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* col, int64_t n, int64_t m,
-                              uint32_t flags) {
+                              uint32_t flags, int64_t col_bound) {
+  if (col_bound < 0) col_bound = n;
   g->n = n;
   g->m = m;
   g->symmetric = (flags & ATOS_GRAPH_SYMMETRIC) != 0;
@@ -191,7 +194,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
   CK(cudaMemset(g->d_scratch, 0, 256));
   if (flags & ATOS_GRAPH_VALIDATE) {
     unsigned int* bad = reinterpret_cast<unsigned int*>(g->d_scratch);
-    k_validate<<<grid_for(std::max(n, m), 256, g->sms), 256>>>(g->d_off, g->d_col, n, m, bad);
+    k_validate<<<grid_for(std::max(n, m), 256, g->sms), 256>>>(g->d_off, g->d_col, n, m, col_bound, bad);
     unsigned int hbad = 0;
     CK(cudaMemcpy(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost));
     if (hbad)
@@ -204,12 +207,12 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     constexpr uint64_t HOT_MAX = 1024;
     uint32_t* indeg = nullptr;
     unsigned long long* hist = nullptr;
-    CK(cudaMalloc(&indeg, (size_t)n * sizeof(uint32_t)));
+    CK(cudaMalloc(&indeg, (size_t)col_bound * sizeof(uint32_t)));
     CK(cudaMalloc(&hist, 32 * sizeof(unsigned long long)));
-    CK(cudaMemset(indeg, 0, (size_t)n * sizeof(uint32_t)));
+    CK(cudaMemset(indeg, 0, (size_t)col_bound * sizeof(uint32_t)));
     CK(cudaMemset(hist, 0, 32 * sizeof(unsigned long long)));
     k_indeg<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, indeg);
-    k_indeg_hist<<<grid_for(n, 256, g->sms), 256>>>(indeg, n, hist);
+    k_indeg_hist<<<grid_for(col_bound, 256, g->sms), 256>>>(indeg, col_bound, hist);
     unsigned long long h[32];
     CK(cudaMemcpy(h, hist, sizeof h, cudaMemcpyDeviceToHost));
     int b = 31;
@@ -268,7 +271,7 @@ extern "C" atos_status atos_graph_create(const int64_t* off, const int32_t* col,
   if (n >= 0x7FFFFFFFLL) return atos_set_error(ATOS_ERR_UNSUPPORTED, "n >= 2^31-1 (bit 31 tags colouring tasks)");
   atos_graph g = new (std::nothrow) atos_graph_s();
   if (!g) return atos_set_error(ATOS_ERR_OUT_OF_MEMORY, "host allocation");
-  atos_status s = graph_init_common(g, off, col, n, m, flags);
+  atos_status s = graph_init_common(g, off, col, n, m, flags, n);
   if (s != ATOS_OK) {
     graph_free(g);
     return s;
@@ -585,7 +588,7 @@ atos_status bfs_local(LaunchCtx& c, int64_t src, const atos_config& cfg);
 extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t* depth_out, atos_stats* st) {
   LaunchCtx c;
   CKS(begin_call(g, cfg, c, st));
-  if (g->comm) return dist_bfs(g, src, &c.cfg, depth_out, st);
+  if (g->dist) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "partitioned graph: use atos_part_*");
   const int64_t n = g->n;
   if (n == 0) return ATOS_OK;
   if (src < 0 || src >= n) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "src %lld not in [0, %lld)", (long long)src, (long long)n);
@@ -685,7 +688,7 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   CKS(begin_call(g, cfg, c, st));
   if (!(alpha > 0.f && alpha < 1.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "alpha not in (0,1)");
   if (!(eps > 0.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "eps <= 0 or NaN");
-  if (g->comm) return dist_pagerank(g, alpha, eps, &c.cfg, rank_out, st);
+  if (g->dist) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "partitioned graph: use atos_part_*");
   const int64_t n = g->n;
   if (n == 0) return ATOS_OK;
   if (!rank_out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "rank_out == NULL");
@@ -735,7 +738,7 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
                                   atos_stats* st) {
   LaunchCtx c;
   CKS(begin_call(g, cfg, c, st));
-  if (g->comm) return atos_set_error(ATOS_ERR_UNSUPPORTED, "colouring is single-GPU (SURVEY §8e: replicas only)");
+  if (g->dist) return atos_set_error(ATOS_ERR_UNSUPPORTED, "colouring is single-GPU (SURVEY §8e: replicas only)");
   if (!g->symmetric) return atos_set_error(ATOS_ERR_INVALID_GRAPH, "atos_color needs ATOS_GRAPH_SYMMETRIC");
   if (c.cfg.gc_literal) return atos_set_error(ATOS_ERR_UNSUPPORTED, "paper-literal colouring (livelocks, R13) not built");
   const int64_t n = g->n;
@@ -796,3 +799,5 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
   if (st) st->num_colors = hmx + 1;
   return ATOS_OK;
 }
+
+#include "dist_impl.cuh"

@@ -33,7 +33,7 @@ struct Workspace {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
-struct DistState;  // dist.cu
+struct DistState;  // dist_impl.cuh
 
 struct atos_graph_s {
   int64_t n = 0;  // local vertex count (== global n when not partitioned)
@@ -49,18 +49,14 @@ struct atos_graph_s {
   int device = 0;
   int sms = 0;
   Workspace ws;
-  // multi-GPU partition (dist.cu)
-  atos_comm comm = nullptr;
+  // multi-GPU partition (dist_impl.cuh)
   int64_t global_n = 0, v_begin = 0, v_end = 0;
   DistState* dist = nullptr;
 };
 
 atos_status atos_set_error(atos_status s, const char* fmt, ...);
 atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* col, int64_t n, int64_t m,
-                              uint32_t flags);
+                              uint32_t flags, int64_t col_bound);
 atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, uint64_t default_cap, bool need_ring,
                        cudaStream_t s);
-atos_status dist_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t* depth_out, atos_stats* st);
-atos_status dist_pagerank(atos_graph g, float alpha, float eps, const atos_config* cfg, float* rank_out,
-                          atos_stats* st);
 void dist_free(atos_graph g);

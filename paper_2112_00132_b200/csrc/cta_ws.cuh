@@ -218,7 +218,7 @@ __device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queu
             comb.key[h] = SmemComb<Payload>::EMPTY;
             comb.val[h] = Payload(0);
             act[0] = app.decide(c, w, 0, app.issue(c, w, 0));
-            item[0] = w;
+            item[0] = app.item_of(w);
           }
           pushed += sink.template warp_push_multi<1>(act, item);
         }

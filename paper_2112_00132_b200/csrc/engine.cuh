@@ -34,6 +34,7 @@ struct GraphView {
 // (strict, R2).
 struct BfsApp {
   static constexpr bool kCombine = false;
+  __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   uint32_t* dist;
   uint32_t* done;  // done[v] = smallest depth at which v has been expanded (init MAX)
   int filter;
@@ -108,6 +109,7 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 template <class R>
 struct PrAppT {
   static constexpr bool kCombine = true;
+  __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   double* rank;
   R* res;
   R alpha, eps;
@@ -158,6 +160,7 @@ struct PrAppT {
 template <class R>
 struct PrBspAppT {
   static constexpr bool kCombine = false;
+  __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   PrAppT<R> base;
   using Payload = R;
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
@@ -440,7 +443,10 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
     bool act[LBS_UNROLL];
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.decide(pk[k], w[k], pr[k], raw[k]);
-    pushed += sink.template warp_push_multi<LBS_UNROLL>(act, w);
+    uint32_t item[LBS_UNROLL];
+#pragma unroll
+    for (int k = 0; k < LBS_UNROLL; ++k) item[k] = app.item_of(w[k]);
+    pushed += sink.template warp_push_multi<LBS_UNROLL>(act, item);
   }
   return pushed;
 }
@@ -534,7 +540,7 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
     const bool v = e < a0;
     int32_t w = v ? ld_stream_s32(g.col + e) : 0;
     bool act = v && app.edge(p, (uint32_t)w);
-    pushed += sink.warp_push(act, (uint32_t)w);
+    pushed += sink.warp_push(act, app.item_of((uint32_t)w));
   }
   const int64_t a1 = a0 + ((e1 - a0) & ~int64_t(3));
   const int4* body = reinterpret_cast<const int4*>(g.col + a0);
@@ -555,14 +561,17 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
     bool act[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) act[k] = v && app.decide(p, w[k], pr[k], raw[k]);
-    pushed += sink.template warp_push_multi<4>(act, w);
+    uint32_t item[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) item[k] = app.item_of(w[k]);
+    pushed += sink.template warp_push_multi<4>(act, item);
   }
   {
     const int64_t e = a1 + lane;
     const bool v = e < e1;
     int32_t w = v ? ld_stream_s32(g.col + e) : 0;
     bool act = v && app.edge(p, (uint32_t)w);
-    pushed += sink.warp_push(act, (uint32_t)w);
+    pushed += sink.warp_push(act, app.item_of((uint32_t)w));
   }
   return pushed;
 }
@@ -633,7 +642,7 @@ __device__ __forceinline__ void thread_batch(const App& app, const GraphView& g,
       ++e;
       act = app.edge(p, (uint32_t)w);
     }
-    pushed += sink.warp_push(act, (uint32_t)w);
+    pushed += sink.warp_push(act, app.item_of((uint32_t)w));
     refill();
   }
   st.edges += edges;
