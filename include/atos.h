@@ -166,8 +166,8 @@ const char* atos_version(void);
  * payload = BFS depth (u32) or PageRank residue contribution (f32 bits).
  * BFS: a remote vertex is sent at most once per improvement (per-rank
  * sent_min filter).  PageRank: remote contributions are accumulated per
- * destination vertex and flushed every round (never thresholded, so no mass
- * is stranded).  Colouring is single-GPU (replicas only). */
+ * destination vertex; a round sends those above eps, and the run closes with
+ * a flush-all round (no mass is stranded).  Colouring is single-GPU (replicas only). */
 
 /* Partitioned graph for rank `rank` of `world`: it owns global vertices
  * [bounds[rank], bounds[rank+1]) (bounds: host int64[world+1], bounds[0] = 0,
@@ -185,8 +185,10 @@ atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, float alpha,
                             const atos_config* cfg);
 /* Run the local persistent kernel to quiescence, then gather this round's
  * outgoing messages.  send_counts: host int64[world] (messages per
- * destination; [rank] is 0). */
-atos_status atos_part_run(atos_graph g, int64_t* send_counts);
+ * destination; [rank] is 0).  PageRank sends only remote accumulations above
+ * eps unless flush_all != 0 (a closing round: everything is sent); the caller
+ * ends a PageRank run only after a flush_all round in which no rank sent. */
+atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* send_counts);
 /* Copy the round's messages, grouped by destination rank in rank order, to
  * dst (host or device, capacity cap messages; cap >= sum(send_counts)). */
 atos_status atos_part_pack(atos_graph g, uint64_t* dst, int64_t cap);

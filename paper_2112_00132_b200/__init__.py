@@ -95,7 +95,7 @@ def lib():
         L.atos_version.restype = ctypes.c_char_p
         L.atos_graph_create_partitioned.argtypes = [i64, i32, i32, vp, vp, vp, i64, u32, ctypes.POINTER(vp)]
         L.atos_part_begin.argtypes = [vp, i32, i64, ctypes.c_float, ctypes.c_float, cfgp]
-        L.atos_part_run.argtypes = [vp, vp]
+        L.atos_part_run.argtypes = [vp, i32, vp]
         L.atos_part_pack.argtypes = [vp, vp, i64]
         L.atos_part_apply.argtypes = [vp, vp, i64]
         L.atos_part_finish.argtypes = [vp, vp, stp]

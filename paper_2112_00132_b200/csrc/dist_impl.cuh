@@ -176,11 +176,14 @@ struct PrPartInitAppT {
   __device__ __forceinline__ bool edge(Payload c, uint32_t w) const { return commit(c, w, 0); }
 };
 
-// Flush remote PR accumulations of destination r's range into messages.
-__global__ void k_pr_flush(float* racc, int64_t b0, int64_t b1, int r, Outbox out) {
+// Flush remote PR accumulations of destination r's range into messages: only
+// those above `thr` (= eps) in a regular round — a smaller amount cannot
+// re-activate its target on its own and keeps accumulating at the sender — and
+// everything (thr = 0) in a closing round, so no mass is stranded.
+__global__ void k_pr_flush(float* racc, int64_t b0, int64_t b1, int r, Outbox out, float thr) {
   for (int64_t w = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < b1; w += (int64_t)gridDim.x * blockDim.x) {
     const float v = racc[w];
-    if (v != 0.0f) {
+    if (v != 0.0f && v > thr) {
       racc[w] = 0.0f;
       out.put(r, ((uint64_t)(uint32_t)(w - b0) << 32) | (uint64_t)__float_as_uint(v));
     }
@@ -387,7 +390,7 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
   return ATOS_OK;
 }
 
-extern "C" atos_status atos_part_run(atos_graph g, int64_t* send_counts) {
+extern "C" atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* send_counts) {
   LaunchCtx c;
   CKS(part_ctx(g, c));
   DistState* d = g->dist;
@@ -411,8 +414,8 @@ extern "C" atos_status atos_part_run(atos_graph g, int64_t* send_counts) {
   if (d->app == 1) {
     for (int r = 0; r < d->world; ++r) {
       if (r == d->rank || d->bounds[r + 1] == d->bounds[r]) continue;
-      k_pr_flush<<<fill_blocks(d->bounds[r + 1] - d->bounds[r], g->sms), 256, 0, c.s>>>(d->racc, d->bounds[r],
-                                                                                       d->bounds[r + 1], r, ob);
+      k_pr_flush<<<fill_blocks(d->bounds[r + 1] - d->bounds[r], g->sms), 256, 0, c.s>>>(
+          d->racc, d->bounds[r], d->bounds[r + 1], r, ob, flush_all ? 0.0f : d->eps);
       c.launches++;
     }
   }

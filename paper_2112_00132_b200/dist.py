@@ -87,8 +87,9 @@ def run(pg: PartGraph, app: int, src: int = 0, alpha: float = 0.85, eps: float =
     dev = torch.device("cpu") if host else torch.device("cuda", torch.cuda.current_device())
     _check(L.atos_part_begin(pg.h, app, src, alpha, eps, ctypes.byref(c)), "atos_part_begin")
     counts = np.zeros(world, dtype=np.int64)
+    flush_all = 0
     while True:
-        _check(L.atos_part_run(pg.h, counts.ctypes.data), "atos_part_run")
+        _check(L.atos_part_run(pg.h, flush_all, counts.ctypes.data), "atos_part_run")
         if world == 1:
             break
         send_counts = torch.from_numpy(counts.copy()).to(dev)
@@ -97,7 +98,11 @@ def run(pg: PartGraph, app: int, src: int = 0, alpha: float = 0.85, eps: float =
         total = send_counts.sum().reshape(1)
         dist.all_reduce(total, group=group)
         if int(total.item()) == 0:
-            break
+            if app == APP_BFS or flush_all:
+                break
+            flush_all = 1  # PageRank: close with a round that sends every pending contribution
+            continue
+        flush_all = 0
         ns = int(counts.sum())
         send = torch.empty(max(ns, 1), dtype=torch.int64, device=dev)
         _check(L.atos_part_pack(pg.h, _ptr(send), ns), "atos_part_pack")

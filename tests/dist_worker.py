@@ -45,7 +45,7 @@ class FakeLib:
             s["q"].append(src - vb)
         return 0
 
-    def atos_part_run(self, h, counts_p):
+    def atos_part_run(self, h, flush_all, counts_p):
         import ctypes
         s = self._get(h)
         vb, ve, b = s["b"][s["rank"]], s["b"][s["rank"] + 1], s["b"]
