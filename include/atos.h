@@ -183,9 +183,11 @@ atos_status atos_graph_create_partitioned(int64_t global_n, int32_t world, int32
  * state (timed into the first round's stats). */
 atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, float alpha, float eps,
                             const atos_config* cfg);
-/* Run the local persistent kernel to quiescence, then gather this round's
- * outgoing messages.  send_counts: host int64[world] (messages per
- * destination; [rank] is 0).  PageRank sends only remote accumulations above
+/* One exchange round: run the local queue kernel — persistent: to local
+ * quiescence; discrete (cfg.kernel): one superstep over the current snapshot —
+ * then gather the round's outgoing messages.  send_counts: host
+ * int64[world + 1]: messages per destination ([rank] is 0) and, at [world],
+ * local tasks still queued (0 for persistent).  PageRank sends only remote accumulations above
  * eps unless flush_all != 0 (a closing round: everything is sent); the caller
  * ends a PageRank run only after a flush_all round in which no rank sent. */
 atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* send_counts);

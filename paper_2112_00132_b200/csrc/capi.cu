@@ -450,7 +450,8 @@ static atos_status host_timeout(LaunchCtx& c) {
 
 // Discrete scheduler: one launch per round over the queue snapshot [h, t).
 template <class P, class App, int W>
-static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0) {
+static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0, uint64_t h0 = 0,
+                                  int64_t max_rounds = -1, uint64_t* h_end = nullptr) {
   auto kern = k_discrete<P, App, W>;
   const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads);
   const size_t smem = worker_smem_bytes<P>(W, F, T);
@@ -458,9 +459,9 @@ static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_
   CKS(set_smem(kern, smem));
   const uint64_t chunk = (W == W_CTA) ? (uint64_t)F : (W == W_WARP ? (uint64_t)F : 32ull * (uint64_t)F);
   const uint64_t per_block = (W == W_CTA) ? 1 : (uint64_t)(T / 32);
-  uint64_t h = 0, t = t0;
+  uint64_t h = h0, t = t0;
   uint64_t* h_tail = &c.g->ws.h_ctl->tail.v;
-  while (h < t) {
+  while (h < t && max_rounds-- != 0) {
     const uint64_t workers = (t - h + chunk - 1) / chunk;
     uint64_t blocks = (workers + per_block - 1) / per_block;
     blocks = std::min<uint64_t>(blocks, 1u << 30);
@@ -478,15 +479,17 @@ static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_
     h = t;
     t = *h_tail;
   }
+  if (h_end) *h_end = h;
   return ATOS_OK;
 }
 
 template <class P, class App>
-static atos_status run_discrete(LaunchCtx& c, const App& app, const Queue& q, uint64_t t0) {
+static atos_status run_discrete(LaunchCtx& c, const App& app, const Queue& q, uint64_t t0, uint64_t h0 = 0,
+                                int64_t max_rounds = -1, uint64_t* h_end = nullptr) {
   switch (c.cfg.worker) {
-    case ATOS_WORKER_THREAD: return run_discrete_w<P, App, W_THREAD>(c, app, q, t0);
-    case ATOS_WORKER_WARP: return run_discrete_w<P, App, W_WARP>(c, app, q, t0);
-    default: return run_discrete_w<P, App, W_CTA>(c, app, q, t0);
+    case ATOS_WORKER_THREAD: return run_discrete_w<P, App, W_THREAD>(c, app, q, t0, h0, max_rounds, h_end);
+    case ATOS_WORKER_WARP: return run_discrete_w<P, App, W_WARP>(c, app, q, t0, h0, max_rounds, h_end);
+    default: return run_discrete_w<P, App, W_CTA>(c, app, q, t0, h0, max_rounds, h_end);
   }
 }
 

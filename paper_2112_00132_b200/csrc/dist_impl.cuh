@@ -245,6 +245,7 @@ struct DistState {
   int64_t rounds = 0, bytes_sent = 0, launches = 0;
   double ms = 0, kernel_ms = 0;
   bool r64 = false;
+  uint64_t next_h = 0;  // discrete rounds: first unprocessed queue position
 };
 
 void dist_free(atos_graph g) {
@@ -335,8 +336,9 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
   if (app == 0 && (src < 0 || src >= g->global_n)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "src out of range");
   if (app == 1 && (!(alpha > 0.f && alpha < 1.f) || !(eps > 0.f)))
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "alpha/eps");
-  if (c.cfg.kernel != ATOS_KERNEL_PERSISTENT)
-    return atos_set_error(ATOS_ERR_UNSUPPORTED, "partitioned runs use the persistent kernel");
+  if (c.cfg.kernel == ATOS_KERNEL_BSP)
+    return atos_set_error(ATOS_ERR_UNSUPPORTED, "partitioned runs use the persistent or discrete kernel");
+  d->next_h = 0;
   d->app = app;
   d->alpha = alpha;
   d->eps = eps;
@@ -401,15 +403,26 @@ extern "C" atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* s
   CK(cudaEventRecord(w.ev[0], c.s));
   Queue q = make_queue(g, c.cfg, (uint32_t)d->app);
   const uint32_t vb = (uint32_t)g->v_begin, ve = (uint32_t)g->v_end;
+  // persistent: drain the local queue to quiescence; discrete: process the
+  // current snapshot [next_h, tail) once (one superstep per exchange round)
+  const bool disc = c.cfg.kernel == ATOS_KERNEL_DISCRETE;
+  uint64_t tail_now = 0;
+  if (disc) {
+    CK(cudaMemcpyAsync(&w.h_ctl->tail.v, &w.ctl->tail.v, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+    CK(cudaStreamSynchronize(c.s));
+    tail_now = w.h_ctl->tail.v;
+  }
+  auto go = [&](const auto& app) -> atos_status {
+    using A = std::decay_t<decltype(app)>;
+    if (disc) return run_discrete<EdgeMapPolicy<A>>(c, app, q, tail_now, d->next_h, 1, &d->next_h);
+    return run_persistent<EdgeMapPolicy<A>>(c, app, q);
+  };
   if (d->app == 0) {
-    BfsPartApp app{w.u32a, w.u32b, d->sent_min, c.cfg.bfs_filter, vb, ve, d->d_bounds, d->world, ob};
-    CKS(run_persistent<EdgeMapPolicy<BfsPartApp>>(c, app, q));
+    CKS(go(BfsPartApp{w.u32a, w.u32b, d->sent_min, c.cfg.bfs_filter, vb, ve, d->d_bounds, d->world, ob}));
   } else if (d->r64) {
-    PrPartAppT<double> app{w.f64a, w.f64b, (double)d->alpha, (double)d->eps, vb, ve, d->racc};
-    CKS(run_persistent<EdgeMapPolicy<PrPartAppT<double>>>(c, app, q));
+    CKS(go(PrPartAppT<double>{w.f64a, w.f64b, (double)d->alpha, (double)d->eps, vb, ve, d->racc}));
   } else {
-    PrPartAppT<float> app{w.f64a, w.f32b, d->alpha, d->eps, vb, ve, d->racc};
-    CKS(run_persistent<EdgeMapPolicy<PrPartAppT<float>>>(c, app, q));
+    CKS(go(PrPartAppT<float>{w.f64a, w.f32b, d->alpha, d->eps, vb, ve, d->racc}));
   }
   if (d->app == 1) {
     for (int r = 0; r < d->world; ++r) {
@@ -436,6 +449,8 @@ extern "C" atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* s
     send_counts[r] = (int64_t)d->h_cnt[r];
     d->bytes_sent += (int64_t)d->h_cnt[r] * 8;
   }
+  // local work still queued (discrete rounds leave the next superstep queued)
+  send_counts[d->world] = disc ? (int64_t)(w.h_ctl->tail.v - d->next_h) : 0;
   return ATOS_OK;
 }
 

@@ -86,16 +86,19 @@ def run(pg: PartGraph, app: int, src: int = 0, alpha: float = 0.85, eps: float =
     host = (dist.get_backend(group) == "gloo") if world > 1 else True
     dev = torch.device("cpu") if host else torch.device("cuda", torch.cuda.current_device())
     _check(L.atos_part_begin(pg.h, app, src, alpha, eps, ctypes.byref(c)), "atos_part_begin")
-    counts = np.zeros(world, dtype=np.int64)
+    counts_all = np.zeros(world + 1, dtype=np.int64)  # [world] = local tasks still queued
+    counts = counts_all[:world]
     flush_all = 0
     while True:
-        _check(L.atos_part_run(pg.h, flush_all, counts.ctypes.data), "atos_part_run")
+        _check(L.atos_part_run(pg.h, flush_all, counts_all.ctypes.data), "atos_part_run")
         if world == 1:
-            break
+            if counts_all[world] == 0:
+                break
+            continue
         send_counts = torch.from_numpy(counts.copy()).to(dev)
         recv_counts = torch.empty_like(send_counts)
         dist.all_to_all_single(recv_counts, send_counts, group=group)
-        total = send_counts.sum().reshape(1)
+        total = torch.tensor([int(counts_all.sum())], dtype=torch.int64, device=dev)
         dist.all_reduce(total, group=group)
         if int(total.item()) == 0:
             if app == APP_BFS or flush_all:
@@ -103,6 +106,7 @@ def run(pg: PartGraph, app: int, src: int = 0, alpha: float = 0.85, eps: float =
             flush_all = 1  # PageRank: close with a round that sends every pending contribution
             continue
         flush_all = 0
+
         ns = int(counts.sum())
         send = torch.empty(max(ns, 1), dtype=torch.int64, device=dev)
         _check(L.atos_part_pack(pg.h, _ptr(send), ns), "atos_part_pack")

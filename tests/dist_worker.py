@@ -64,8 +64,8 @@ class FakeLib:
                     r = int(np.searchsorted(b, w, side="right") - 1)
                     out[r].append(((w - int(b[r])) << 32) | int(d))
         s["out"] = out
-        c = np.ctypeslib.as_array(ctypes.cast(counts_p, ctypes.POINTER(ctypes.c_int64)), (s["world"],))
-        c[:] = [len(o) for o in out]
+        c = np.ctypeslib.as_array(ctypes.cast(counts_p, ctypes.POINTER(ctypes.c_int64)), (s["world"] + 1,))
+        c[:] = [len(o) for o in out] + [0]
         return 0
 
     def atos_part_pack(self, h, dst, cap):
@@ -118,15 +118,16 @@ def main():
         atos._lib = fake
         adist.lib = lambda: fake
         atos.lib = lambda: fake
-    else:
+    else:  # "gpu" / "gpu-discrete": every rank on cuda:0
         torch.cuda.set_device(0)
     g, fwd = gg.permute(gg.rmat(12, 8, seed=3), 7)
     src = int(fwd[0])
     pg = adist.PartGraph.from_global(g, world, rank)
+    kern = "discrete" if mode == "gpu-discrete" else "persistent"
     if app == 0:
-        res, st = adist.bfs(pg, src, timeout_s=60) if mode == "gpu" else adist.bfs(pg, src)
+        res, st = adist.bfs(pg, src, timeout_s=60, kernel=kern) if mode != "fake" else adist.bfs(pg, src)
     else:
-        res, st = adist.pagerank(pg, 0.85, 1e-6, timeout_s=60)
+        res, st = adist.pagerank(pg, 0.85, 1e-6, timeout_s=60, kernel=kern)
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), res=res, rounds=st.get("rounds", 0),
              bytes=st.get("bytes_sent", 0), src=src)
     dist.barrier()

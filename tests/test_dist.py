@@ -66,18 +66,18 @@ def test_orchestration_gloo_fake_engine(world, tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_gpu_partitioned_bfs_multiprocess(world, tmp_path):
-    depth, parts = _spawn(world, "gpu", 0, tmp_path)
+@pytest.mark.parametrize("world,mode", [(2, "gpu"), (3, "gpu"), (3, "gpu-discrete")])
+def test_gpu_partitioned_bfs_multiprocess(world, mode, tmp_path):
+    depth, parts = _spawn(world, mode, 0, tmp_path)
     g, fwd = gg.permute(gg.rmat(12, 8, seed=3), 7)
     assert np.array_equal(depth, oracle.bfs(g, int(parts[0]["src"])))
     assert sum(int(p["bytes"]) for p in parts) > 0  # remote traffic happened
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_gpu_partitioned_pagerank_multiprocess(world, tmp_path):
-    rank, parts = _spawn(world, "gpu", 1, tmp_path)
+@pytest.mark.parametrize("world,mode", [(2, "gpu"), (3, "gpu"), (2, "gpu-discrete")])
+def test_gpu_partitioned_pagerank_multiprocess(world, mode, tmp_path):
+    rank, parts = _spawn(world, mode, 1, tmp_path)
     g, fwd = gg.permute(gg.rmat(12, 8, seed=3), 7)
     x, _ = oracle.pagerank(g, 0.85)
     assert np.max(np.abs(rank - x)) / x.max() <= 1e-4

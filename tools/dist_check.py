@@ -15,3 +15,7 @@ for it in range(2):
     r2, st2 = adist.pagerank(pg, 0.85, 1e-6)
     print("part1 ", {k: st2[k] for k in ("ms", "tasks_popped", "edges_processed", "chunk_tasks", "rounds")})
 print("maxdiff", float(np.max(np.abs(r - r2))))
+for k in ("persistent", "discrete"):
+    for it in range(2):
+        r3, st3 = adist.pagerank(pg, 0.85, 1e-6, kernel=k)
+        print("part1", k, {kk: st3[kk] for kk in ("ms", "tasks_popped", "edges_processed", "rounds")})
