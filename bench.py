@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--pr-fetch", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-kernel", default="persistent", choices=["persistent", "discrete"],
+                    help="N > 1: per-round local strategy (persistent = drain to local quiescence)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: host-staged exchange, for 1-GPU smoke tests)")
     return ap.parse_args()
@@ -320,7 +322,7 @@ def run_atos_multi(args, rank, world, local_rank):
     src = int(fwd[0])
     del g0
     pg = adist.PartGraph.from_global(g, world, rank)
-    cfg = atos.Config(kernel="persistent", worker="cta", fetch_size=args.fetch, cta_threads=args.threads,
+    cfg = atos.Config(kernel=args.dist_kernel, worker="cta", fetch_size=args.fetch, cta_threads=args.threads,
                       timeout_s=300)
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -367,9 +369,10 @@ def run_atos_multi(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": tot_ms / len(recs), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32+f32", "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_bfs0+pagerank", "scale": args.scale,
-                   "edge_factor": args.edge_factor, "n": g.n, "m": g.m, "kernel": "persistent", "worker": "cta",
-                   "fetch_size": args.fetch, "cta_threads": args.threads, "alpha": ALPHA, "eps": EPS,
-                   "parallelism": f"1d-partition x{world} (permuted ids, NCCL all-to-all per round)",
+                   "edge_factor": args.edge_factor, "n": g.n, "m": g.m, "kernel": args.dist_kernel,
+                   "worker": "cta", "fetch_size": args.fetch, "cta_threads": args.threads, "alpha": ALPHA,
+                   "eps": EPS, "backend": args.backend,
+                   "parallelism": f"1d-partition x{world} (permuted ids, all-to-all per round)",
                    "l2": "flushed (512 MB write) between steps; inputs > L2"},
         "bfs": {"gteps": e_bfs / (float(t[1].item()) / len(recs) * 1e-3) / 1e9, "ms": float(t[1].item()) / len(recs),
                 "rounds": int(loc[2].item()) // world},
