@@ -661,6 +661,15 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
   c.launches += bsp ? 4 : 5;
   CK(cudaEventRecord(w.ev[1], c.s));
   PrAppT<R> app{rank, res, (R)alpha, (R)eps};
+  if (c.cfg.pr_activation == 1) {
+    if constexpr (std::is_same<R, float>::value) {
+      // f1: Alg. 4's Check_Size window activation; every vertex starts queued
+      k_fill<uint32_t><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, n, 1u);
+      PrWindowAppT<float> wapp{rank, res, w.u32a, alpha, eps, n, c.cfg.check_size};
+      CKS(run_persistent<EdgeMapPolicy<PrWindowAppT<float>>>(c, wapp, make_queue(g, c.cfg, 1)));
+      return ATOS_OK;
+    }
+  }
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
     CKS(run_persistent<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1)));
   } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
@@ -695,7 +704,10 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   const int64_t n = g->n;
   if (n == 0) return ATOS_OK;
   if (!rank_out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "rank_out == NULL");
-  if (c.cfg.pr_activation == 1) return atos_set_error(ATOS_ERR_UNSUPPORTED, "Check_Size window activation not built");
+  if (c.cfg.pr_activation == 1 && (c.cfg.kernel != ATOS_KERNEL_PERSISTENT || c.cfg.worker != ATOS_WORKER_CTA ||
+                                   c.cfg.pr_residue_fp64))
+    return atos_set_error(ATOS_ERR_UNSUPPORTED,
+                          "Check_Size window activation is built for persistent CTA workers with fp32 residues");
   Workspace& w = g->ws;
   const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
   const bool r64 = c.cfg.pr_residue_fp64 != 0;
@@ -706,6 +718,7 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
                           (unsigned long long)w.cap, (long long)n);
   CKS(ensure(w.f32a, w.f32a_n, (size_t)n));
   CKS(ensure(w.f64a, w.f64a_n, (size_t)n));
+  if (c.cfg.pr_activation == 1) CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // queued flags
   if (r64) CKS(ensure(w.f64b, w.f64b_n, (size_t)n));
   else CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
   if (bsp) {

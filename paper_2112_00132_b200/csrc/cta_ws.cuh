@@ -134,6 +134,109 @@ __device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g
   __syncwarp();
 }
 
+// Check_Size window sweep (f1): the warp reserves `span` ids from the global
+// cursor and pushes every id with residue > eps that is not already queued.
+// Returns the number pushed (warp-uniform).  ctl->aux[0] = cursor,
+// aux[1] = cursor position of the last push, aux[2] = cursor at the last
+// completed task.
+template <class App>
+__device__ __forceinline__ uint32_t window_sweep(const App& app, const Queue& q, uint32_t span);
+
+// Warp-collective pop for window activation: try the queue; on a failed pop
+// sweep one window (the paper's f2 hook continues the check sweep); quit on a
+// clean full sweep with an empty queue (R9).  Per successful pop the warp also
+// sweeps n * Check_Size ids (Alg. 4: every popped vertex checks a window).
+template <class App>
+__device__ __forceinline__ uint32_t window_pop(const App& app, const Queue& q, uint32_t want, uint64_t& first,
+                                               uint64_t& hw) {
+  unsigned ns = 0;
+  for (;;) {
+    uint32_t n = 0;
+    uint64_t qlen = 0;
+    if (lane_id() == 0) {
+      n = q_aborted(q) || q_timed_out(q) ? 0xFFFFFFFFu : q_try_pop(q, want, first, qlen);
+      if (n && n != 0xFFFFFFFFu && qlen > hw) hw = qlen;
+    }
+    n = __shfl_sync(FULL_MASK, n, 0);
+    first = __shfl_sync(FULL_MASK, first, 0);
+    if (n == 0xFFFFFFFFu) return 0;
+    if (n) return n;
+    if (window_sweep(app, q, 32u * (uint32_t)app.check_size)) {
+      ns = 0;
+      continue;
+    }
+    // Termination (R9): with the queue empty, one warp (lock aux[3]: 0 -> 1)
+    // sweeps ALL n residues itself; if it finds none > eps and the queue stayed
+    // empty and unchanged (no task could run, so residues were stable) the run
+    // is over (aux[3] = 2).
+    int state = 0;  // 0 = keep going, 1 = sweeper, 2 = quit
+    uint64_t t0 = 0;
+    if (lane_id() == 0) {
+      const uint64_t flag = ld_relaxed_u64(&q.ctl->aux[3].v);
+      if (flag == 2) {
+        state = 2;
+      } else {
+        const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
+        t0 = ld_relaxed_u64(&q.ctl->tail.v);
+        if (p == t0 && atomicCAS(reinterpret_cast<unsigned long long*>(&q.ctl->aux[3].v), 0ull, 1ull) == 0ull) state = 1;
+      }
+    }
+    state = __shfl_sync(FULL_MASK, state, 0);
+    if (state == 2) return 0;
+    if (state == 1) {
+      uint32_t found = 0;
+      for (int64_t b = 0; b < app.n; b += 32) {
+        const int64_t v = b + lane_id();
+        bool act = false;
+        if (v < app.n) {
+          const float r = __ldcg(reinterpret_cast<const float*>(app.res) + v);
+          act = r > (float)app.eps && atomicExch(app.queued + v, 1u) == 0u;
+        }
+        found += q_warp_push(q, act, (uint32_t)v);
+      }
+      bool done = false;
+      if (lane_id() == 0) {
+        __threadfence();
+        const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
+        const uint64_t t = ld_relaxed_u64(&q.ctl->tail.v);
+        done = found == 0 && p == t && t == t0;
+        st_relaxed_u64(&q.ctl->aux[3].v, done ? 2ull : 0ull);
+      }
+      if (__shfl_sync(FULL_MASK, done, 0)) return 0;
+      ns = 0;
+      continue;
+    }
+    if (ns) __nanosleep(ns);
+    ns = ns == 0 ? 32 : (ns < 256 ? ns * 2 : ns);
+  }
+}
+
+template <class App>
+__device__ __forceinline__ uint32_t window_sweep(const App& app, const Queue& q, uint32_t span) {
+  uint64_t s = 0;
+  if (lane_id() == 0) s = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->aux[0].v), (unsigned long long)span);
+  s = __shfl_sync(FULL_MASK, s, 0);
+  uint32_t pushed = 0;
+  constexpr int G = 8;
+  for (uint32_t i = 0; i < span; i += 32 * G) {
+    float r[G];
+    uint32_t v[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const uint32_t j = i + lane_id() + 32 * k;
+      v[k] = (uint32_t)((s + j) % (uint64_t)app.n);
+      r[k] = j < span ? __ldcg(reinterpret_cast<const float*>(app.res) + v[k]) : 0.f;
+    }
+    bool act[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) act[k] = r[k] > (float)app.eps && atomicExch(app.queued + v[k], 1u) == 0u;
+    pushed += q_warp_push_multi<G>(q, act, v);
+  }
+  if (pushed && lane_id() == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&q.ctl->aux[1].v), (unsigned long long)(s + span));
+  return pushed;
+}
+
 template <class App>
 __device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queue& q, int F, unsigned char* smem,
                                   LocalStats& st) {
@@ -153,9 +256,13 @@ __device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queu
       if (round >= 2) bar_sync_n(3 + b, T);  // workers released buffer b
       uint64_t first = 0;
       uint32_t n = 0;
-      if (lane == 0) n = q_pop_or_quit(q, (uint32_t)F, first, st.hw);
-      n = __shfl_sync(FULL_MASK, n, 0);
-      first = __shfl_sync(FULL_MASK, first, 0);
+      if constexpr (App::kWindow) {
+        n = window_pop(app, q, (uint32_t)F, first, st.hw);
+      } else {
+        if (lane == 0) n = q_pop_or_quit(q, (uint32_t)F, first, st.hw);
+        n = __shfl_sync(FULL_MASK, n, 0);
+        first = __shfl_sync(FULL_MASK, first, 0);
+      }
       int64_t* e0 = buf_e0(b);
       int64_t* pre = buf_pre(b);
       Payload* pay = buf_pay(b);
@@ -204,6 +311,12 @@ __device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queu
       pushed += lbs_expand(app, g, sink, pre, buf_e0(b), buf_pay(b), (int)n, total, wid - 1, nw, comb);
       edges += total;
       bar_sync_n(5, T - 32);  // every worker's pushes for this batch are reserved
+      if constexpr (App::kWindow) {
+        // Alg. 4 lines 11-14: each popped vertex checks a Check_Size window;
+        // the batch's n * Check_Size ids are split over the worker warps
+        pushed += window_sweep(app, q, (n * (uint32_t)app.check_size + nw - 1) / nw);
+        bar_sync_n(5, T - 32);
+      }
       if constexpr (App::kCombine) {
         // flush: one global atomic per combined destination; push on a crossing
         const uint32_t nu = *comb.nused;
@@ -227,6 +340,11 @@ __device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queu
       }
       if (tid == 32) {
         st.popped += n;
+        if constexpr (App::kWindow) {  // this batch's residue adds precede the sweep positions after it
+          __threadfence();
+          atomicMax(reinterpret_cast<unsigned long long*>(&q.ctl->aux[2].v),
+                    (unsigned long long)ld_relaxed_u64(&q.ctl->aux[0].v));
+        }
         q_done(q, n);
         q_trace(q, n, (uint64_t)total);
       }

@@ -37,6 +37,7 @@ struct Outbox {
 // sends so a remote vertex is sent once per improvement of its tentative depth.
 struct BfsPartApp {
   static constexpr bool kCombine = false;
+  static constexpr bool kWindow = false;
   uint32_t* dist;
   uint32_t* done;
   uint32_t* sent_min;
@@ -97,6 +98,7 @@ struct BfsPartApp {
 template <class R>
 struct PrPartAppT {
   static constexpr bool kCombine = true;
+  static constexpr bool kWindow = false;
   double* rank;
   R* res;
   R alpha, eps;
@@ -149,6 +151,7 @@ struct PrPartAppT {
 template <class R>
 struct PrPartInitAppT {
   static constexpr bool kCombine = false;
+  static constexpr bool kWindow = false;
   R* res;
   float* racc;
   R c0;

@@ -34,6 +34,7 @@ struct GraphView {
 // (strict, R2).
 struct BfsApp {
   static constexpr bool kCombine = false;
+  static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   uint32_t* dist;
   uint32_t* done;  // done[v] = smallest depth at which v has been expanded (init MAX)
@@ -109,6 +110,7 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 template <class R>
 struct PrAppT {
   static constexpr bool kCombine = true;
+  static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   double* rank;
   R* res;
@@ -155,11 +157,72 @@ struct PrAppT {
   }
 };
 
+// Asynchronous PageRank with the paper's own activation rule (Alg. 4 lines
+// 11-14): residue adds are fire-and-forget
+// (`red`, no threshold test per edge) and vertices are (re)activated by a
+// sweeping window — each worker reserves Check_Size ids from a global cursor
+// (atomicAdd(check, Check_Size)) and pushes those with residue > eps (R6/R7,
+// check_id mod n).  queued[v] keeps a vertex in the queue at most once (set on
+// push, cleared at pop before the residue exchange).  Termination (R9): the
+// queue is empty AND the cursor has swept n ids since the last push and the
+// last completed task — a clean full sweep over unchanging residues.
+template <class R>
+struct PrWindowAppT {
+  static constexpr bool kCombine = false;
+  static constexpr bool kWindow = true;
+  double* rank;
+  R* res;
+  uint32_t* queued;
+  R alpha, eps;
+  int64_t n;
+  int check_size;
+  using Payload = R;
+  using Probe = int;
+  using Raw = int;
+  __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
+  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
+  struct Pre {
+    int64_t e0, e1;
+    R r;
+  };
+  __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
+    Pre x;
+    x.e0 = ld_nc_s64(g.off + v);
+    x.e1 = ld_nc_s64(g.off + v + 1);
+    atomicExch(queued + v, 0u);  // a later sweep may re-queue v
+    x.r = atomic_take(res + v);
+    return x;
+  }
+  __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
+    if (x.r == R(0)) return false;
+    atomicAdd(rank + v, (double)x.r);
+    if (x.e1 == x.e0) return false;
+    p = alpha * x.r / (R)(x.e1 - x.e0);
+    return true;
+  }
+  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1, Payload& p) const {
+    Pre x = begin_load(v, g);
+    e0 = x.e0;
+    e1 = x.e1;
+    return begin_commit(v, x, p);
+  }
+  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const {
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(res + w), "f"((float)c),
+                 "l"(pol_evict_last()));
+    return 0;
+  }
+  __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe p) const { return decide(c, w, p, issue(c, w, p)); }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const { return commit(c, w, 0); }
+};
+
 // BSP PageRank push kernel body (Alg. 3 lines 11-16): same push
 // but the frontier is rebuilt by the filter kernel, so nothing is appended.
 template <class R>
 struct PrBspAppT {
   static constexpr bool kCombine = false;
+  static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   PrAppT<R> base;
   using Payload = R;

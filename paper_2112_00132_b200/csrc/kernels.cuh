@@ -321,6 +321,7 @@ __global__ void k_bfs_init(uint32_t* dist, uint32_t* done, int64_t n, int64_t sr
 template <class R>
 struct PrInitAppT {
   static constexpr bool kCombine = false;
+  static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   R* res;
   R c0;  // (1 - alpha) * alpha

@@ -215,6 +215,24 @@ def test_pagerank_fp64_residue(atos, worker):
         assert st["max_residue"] <= 1e-6
 
 
+@pytest.mark.parametrize("check_size", [1, 8, 32])
+@pytest.mark.parametrize("gname", ["rmat16", "grid64", "star", "road", "hub", "two"])
+def test_pagerank_window_activation(atos, gname, check_size):
+    """Alg. 4's Check_Size window activation: red adds,
+    sweeping-cursor re-activation, full-sweep termination (R9)."""
+    x = jacobi(gname)
+    r, st = atos.pagerank(D(atos, gname), 0.85, 1e-6, pr_activation=1, check_size=check_size, fetch_size=64)
+    assert np.max(np.abs(r - x)) / x.max() <= PR_TOL
+    assert st["max_residue"] <= 1e-6
+
+
+def test_pagerank_window_unsupported_combos(atos):
+    for kw in [dict(kernel="discrete"), dict(worker="warp"), dict(pr_residue_fp64=True)]:
+        with pytest.raises(atos.AtosError) as e:
+            atos.pagerank(D(atos, "K9"), 0.85, 1e-6, pr_activation=1, **kw)
+        assert e.value.name == "UNSUPPORTED"
+
+
 @pytest.mark.parametrize("gname", ["grid64", "star", "K9", "path", "two", "road", "hub"])
 def test_pagerank_special(atos, gname):
     x = jacobi(gname)

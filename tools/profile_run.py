@@ -15,10 +15,12 @@ ap.add_argument("--kernel", default="persistent")
 ap.add_argument("--fetch", type=int, default=256)
 ap.add_argument("--threads", type=int, default=256)
 ap.add_argument("--filter", type=int, default=1)
+ap.add_argument("--window", type=int, default=0)
+ap.add_argument("--check", type=int, default=8)
 a = ap.parse_args()
 g = gg.grid(a.grid, a.grid) if a.grid else gg.rmat(a.scale, 16, seed=1, symmetrize=(a.app == "color"))
 G = atos.Graph.from_csr(g, symmetric=(a.app == "color"))
-cfg = atos.Config(kernel=a.kernel, worker=a.worker, fetch_size=a.fetch, cta_threads=a.threads, bfs_filter=bool(a.filter), timeout_s=300)
+cfg = atos.Config(kernel=a.kernel, worker=a.worker, fetch_size=a.fetch, cta_threads=a.threads, bfs_filter=bool(a.filter), timeout_s=300, pr_activation=a.window, check_size=a.check)
 for i in range(a.iters):
     if a.app == "bfs":
         d, st = atos.bfs(G, 0, cfg)
