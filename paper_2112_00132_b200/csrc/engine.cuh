@@ -464,16 +464,14 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
   const int lane = lane_id();
   const int64_t stride = (int64_t)nw * 32 * LBS_UNROLL;
   uint32_t pushed = 0;
-  for (int64_t eb = (int64_t)wi * 32 * LBS_UNROLL; eb < total; eb += stride) {
+  // Locate the items of the edges of step `eb` and issue their column loads.
+  auto fetch = [&](int64_t eb, uint32_t (&w)[LBS_UNROLL], int (&idx)[LBS_UNROLL]) {
     const int64_t elast = min(total, eb + 32 * LBS_UNROLL) - 1;
     int bound = 0;
     if (lane == 0) bound = lbs_find(pre, n, eb);
     if (lane == 31) bound = lbs_find(pre, n, elast);
-    const int lo0 = __shfl_sync(FULL_MASK, bound, 0);
+    int lo = __shfl_sync(FULL_MASK, bound, 0);
     const int hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
-    uint32_t w[LBS_UNROLL];
-    int idx[LBS_UNROLL];
-    int lo = lo0;
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k) {
       const int64_t e = eb + lane + 32 * k;
@@ -485,6 +483,23 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
         w[k] = (uint32_t)ld_col_raw(g.col + e0s[lo] + (e - pre[lo]));
       }
     }
+  };
+  // Software pipeline: the next step's column loads are in flight while this
+  // step's probes / atomics / push wait on L2 (two dependent memory latencies
+  // per step otherwise — col load then probe).
+  uint32_t wn[LBS_UNROLL];
+  int idxn[LBS_UNROLL];
+  int64_t eb = (int64_t)wi * 32 * LBS_UNROLL;
+  if (eb < total) fetch(eb, wn, idxn);
+  for (; eb < total; eb += stride) {
+    uint32_t w[LBS_UNROLL];
+    int idx[LBS_UNROLL];
+#pragma unroll
+    for (int k = 0; k < LBS_UNROLL; ++k) {
+      w[k] = wn[k];
+      idx[k] = idxn[k];
+    }
+    if (eb + stride < total) fetch(eb + stride, wn, idxn);
     if (Comb::kOn) {
 #pragma unroll
       for (int k = 0; k < LBS_UNROLL; ++k)
