@@ -1,0 +1,137 @@
+// cta_ws2.cuh — decoupled warp-specialised persistent CTA worker for the
+// edge-map apps (BFS, PageRank; SURVEY §8a rows a4 + a5).
+//
+// Warp 0 (the queue agent) pops FETCH-sized batches, reads their slots, runs
+// begin()/chunk/split and scans degrees into a ring of NBUF shared-memory batch
+// buffers, up to NBUF-1 batches ahead.  Worker warps 1..W-1 consume the ring
+// in order, claiming 32*UNROLL-edge steps of the current batch with a
+// shared-memory atomic; a warp that finds the batch exhausted moves on to the
+// next batch at once — no CTA barrier per batch.  The last warp to leave a
+// batch increments `processed` (a7; every warp's pushes for the batch are
+// reserved before it leaves) and frees the buffer.  (The double-buffered
+// version with bar.sync hand-offs spent 20-27% of its stall samples in
+// barriers, profiles/r01_*_ncu.md.)
+#pragma once
+#include "cta_ws.cuh"
+
+namespace atos {
+
+constexpr int NBUF = 4;
+enum : int { BUF_FREE = 0, BUF_READY = 1, BUF_QUIT = 2 };
+
+struct BufHdr {
+  int state;     // BUF_*
+  int n;         // items
+  int next;      // next step index to claim
+  int left;      // warps that have left this batch
+  long long total;
+};
+
+template <class Payload>
+__host__ __device__ constexpr size_t ws2_smem_bytes(int F) {
+  return (size_t)NBUF * ws_buf_bytes<Payload>(F) + NBUF * sizeof(BufHdr) + 64;
+}
+
+__device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ void vstore(int* p, int v) { *(volatile int*)p = v; }
+
+template <class App>
+__device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Queue& q, int F, unsigned char* smem,
+                                   LocalStats& st) {
+  using Payload = typename App::Payload;
+  const int T = blockDim.x, tid = threadIdx.x, wid = tid >> 5, lane = lane_id();
+  const size_t bb = ws_buf_bytes<Payload>(F);
+  BufHdr* hdr = reinterpret_cast<BufHdr*>(smem + NBUF * bb);
+  auto buf_e0 = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb); };
+  auto buf_pre = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb) + F; };
+  auto buf_pay = [&](int b) { return reinterpret_cast<Payload*>(reinterpret_cast<int64_t*>(smem + b * bb) + 2 * F + 1); };
+  const Queue* cq = q.chunks ? &q : nullptr;
+  const int nw = (T >> 5) - 1;
+  if (tid < NBUF) hdr[tid] = BufHdr{BUF_FREE, 0, 0, 0, 0};
+  __syncthreads();
+
+  if (wid == 0) {
+    // ------------------------------------------------ queue agent
+    for (int b = 0;; b = (b + 1) % NBUF) {
+      // wait until the workers have released buffer b
+      for (unsigned ns = 8; vload(&hdr[b].state) != BUF_FREE; ns = ns < 256 ? ns * 2 : ns) __nanosleep(ns);
+      uint64_t first = 0;
+      uint32_t n = 0;
+      if constexpr (App::kWindow) {
+        n = window_pop(app, q, (uint32_t)F, first, st.hw);
+      } else {
+        if (lane == 0) n = q_pop_or_quit(q, (uint32_t)F, first, st.hw);
+        n = __shfl_sync(FULL_MASK, n, 0);
+        first = __shfl_sync(FULL_MASK, first, 0);
+      }
+      if (n) {
+        agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b));
+        warp_exclusive_scan(buf_pre(b), (int)n);
+      }
+      if (lane == 0) {
+        hdr[b].n = (int)n;
+        hdr[b].total = n ? buf_pre(b)[n] : 0;
+        hdr[b].next = 0;
+        hdr[b].left = 0;
+        __threadfence_block();
+        vstore(&hdr[b].state, n ? BUF_READY : BUF_QUIT);
+      }
+      __syncwarp();
+      if (n == 0) break;
+    }
+  } else {
+    // ------------------------------------------------ edge workers
+    RingSink sink{q};
+    uint32_t pushed = 0;
+    uint64_t edges = 0;
+    for (int b = 0;; b = (b + 1) % NBUF) {
+      int s;
+      for (unsigned ns = 8; (s = vload(&hdr[b].state)) == BUF_FREE; ns = ns < 128 ? ns * 2 : ns) __nanosleep(ns);
+      if (s == BUF_QUIT) break;
+      __threadfence_block();
+      const int n = hdr[b].n;
+      const int64_t total = hdr[b].total;
+      const int64_t* pre = buf_pre(b);
+      const int64_t* e0 = buf_e0(b);
+      const Payload* pay = buf_pay(b);
+      const int64_t steps = (total + 32 * LBS_UNROLL - 1) / (32 * LBS_UNROLL);
+      for (;;) {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(&hdr[b].next, 1);
+        c = __shfl_sync(FULL_MASK, c, 0);
+        if ((int64_t)c >= steps) break;
+        const uint32_t p = lbs_step(app, g, sink, pre, e0, pay, n, total, (int64_t)c * 32 * LBS_UNROLL);
+        if (lane == 0) pushed += p;
+        if (lane == 0) edges += (uint64_t)min((int64_t)32 * LBS_UNROLL, total - (int64_t)c * 32 * LBS_UNROLL);
+      }
+      if constexpr (App::kWindow) {
+        // Alg. 4 lines 11-14: each popped vertex checks a Check_Size window
+        pushed += window_sweep(app, q, ((uint32_t)n * (uint32_t)app.check_size + nw - 1) / nw);
+      }
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&hdr[b].left, 1) == nw - 1;
+      }
+      last = __shfl_sync(FULL_MASK, last, 0);
+      if (last && lane == 0) {
+        st.popped += (uint64_t)n;
+        if constexpr (App::kWindow) {
+          __threadfence();
+          atomicMax(reinterpret_cast<unsigned long long*>(&q.ctl->aux[2].v),
+                    (unsigned long long)ld_relaxed_u64(&q.ctl->aux[0].v));
+        }
+        q_done(q, (uint32_t)n);
+        q_trace(q, (uint32_t)n, (uint64_t)total);
+        vstore(&hdr[b].state, BUF_FREE);
+      }
+    }
+    if (lane == 0) {
+      st.pushed += pushed;
+      st.edges += edges;
+    }
+  }
+}
+
+}  // namespace atos

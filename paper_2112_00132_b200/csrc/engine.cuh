@@ -457,6 +457,52 @@ struct SmemComb {
   }
 };
 
+// One LBS step: the warp expands flattened edges [eb, eb + 32*UNROLL) of a
+// prepared batch (see lbs_expand).  Returns the pushes (warp-uniform).
+template <class App, class Sink>
+__device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
+                                             const int64_t* e0s, const typename App::Payload* pay, int n,
+                                             int64_t total, int64_t eb) {
+  const int lane = lane_id();
+  const int64_t elast = min(total, eb + 32 * LBS_UNROLL) - 1;
+  int bound = 0;
+  if (lane == 0) bound = lbs_find(pre, n, eb);
+  if (lane == 31) bound = lbs_find(pre, n, elast);
+  int lo = __shfl_sync(FULL_MASK, bound, 0);
+  const int hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
+  uint32_t w[LBS_UNROLL];
+  int idx[LBS_UNROLL];
+#pragma unroll
+  for (int k = 0; k < LBS_UNROLL; ++k) {
+    const int64_t e = eb + lane + 32 * k;
+    idx[k] = -1;
+    w[k] = 0;
+    if (e < total) {
+      lo = lbs_find_range(pre, lo, hi, e);
+      idx[k] = lo;
+      w[k] = (uint32_t)ld_stream_s32(g.col + e0s[lo] + (e - pre[lo]));
+    }
+  }
+  typename App::Probe pr[LBS_UNROLL];
+#pragma unroll
+  for (int k = 0; k < LBS_UNROLL; ++k)
+    if (idx[k] >= 0) pr[k] = app.probe(w[k]);
+  typename App::Raw raw[LBS_UNROLL];
+  typename App::Payload pk[LBS_UNROLL];
+#pragma unroll
+  for (int k = 0; k < LBS_UNROLL; ++k) {
+    pk[k] = idx[k] >= 0 ? pay[idx[k]] : typename App::Payload{};
+    if (idx[k] >= 0) raw[k] = app.issue(pk[k], w[k], pr[k]);
+  }
+  bool act[LBS_UNROLL];
+#pragma unroll
+  for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.decide(pk[k], w[k], pr[k], raw[k]);
+  uint32_t item[LBS_UNROLL];
+#pragma unroll
+  for (int k = 0; k < LBS_UNROLL; ++k) item[k] = app.item_of(w[k]);
+  return sink.template warp_push_multi<LBS_UNROLL>(act, item);
+}
+
 template <class App, class Sink, class Comb = NoComb>
 __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
                                                const int64_t* e0s, const typename App::Payload* pay, int n,

@@ -7,7 +7,7 @@
 //   k_bsp         one launch per BSP step over an explicit frontier array
 //                 (Alg. 1/3/5), appending to an out-frontier.
 #pragma once
-#include "cta_ws.cuh"
+#include "cta_ws2.cuh"
 #include "gc.cuh"
 
 namespace atos {
@@ -23,10 +23,10 @@ struct EdgeMapPolicy {
   static constexpr bool kWarpSpecialised = true;
   using Payload = typename App::Payload;
   static __host__ __device__ size_t smem_bytes(int F) { return cta_smem_bytes<Payload>(F); }
-  static __host__ __device__ size_t ws_smem(int F) { return ws_smem_bytes<Payload>(F, App::kCombine); }
+  static __host__ __device__ size_t ws_smem(int F) { return ws2_smem_bytes<Payload>(F); }
   static __device__ __forceinline__ void cta_persistent(const App& app, const GraphView& g, const Queue& q, int F,
                                                         unsigned char* smem, LocalStats& st) {
-    cta_ws_persistent(app, g, q, F, smem, st);
+    cta_ws2_persistent(app, g, q, F, smem, st);
   }
   template <class Src, class Sink>
   static __device__ __forceinline__ void cta(const App& app, const GraphView& g, const Src& src, const Sink& sink,
