@@ -21,6 +21,7 @@ enum : int { BUF_FREE = 0, BUF_READY = 1, BUF_QUIT = 2 };
 
 struct BufHdr {
   int state;     // BUF_*
+  int seq;       // ring pass this batch belongs to (a fast warp must not re-enter an older batch)
   int n;         // items
   int next;      // next step index to claim
   int left;      // warps that have left this batch
@@ -47,14 +48,24 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
   auto buf_pay = [&](int b) { return reinterpret_cast<Payload*>(reinterpret_cast<int64_t*>(smem + b * bb) + 2 * F + 1); };
   const Queue* cq = q.chunks ? &q : nullptr;
   const int nw = (T >> 5) - 1;
-  if (tid < NBUF) hdr[tid] = BufHdr{BUF_FREE, 0, 0, 0, 0};
+  if (tid < NBUF) hdr[tid] = BufHdr{BUF_FREE, -1, 0, 0, 0, 0};
   __syncthreads();
 
   if (wid == 0) {
     // ------------------------------------------------ queue agent
-    for (int b = 0;; b = (b + 1) % NBUF) {
+    for (int i = 0;; ++i) {
+      const int b = i % NBUF;
       // wait until the workers have released buffer b
-      for (unsigned ns = 8; vload(&hdr[b].state) != BUF_FREE; ns = ns < 256 ? ns * 2 : ns) __nanosleep(ns);
+      bool dead = false;
+      for (unsigned ns = 8; vload(&hdr[b].state) != BUF_FREE; ns = ns < 256 ? ns * 2 : ns) {
+        __nanosleep(ns);
+        if (q_aborted(q) || q_timed_out(q)) { dead = true; break; }
+      }
+      if (dead) {  // workers are stuck on an unreleased batch only if they died; publish QUIT anyway
+        if (lane == 0) { hdr[b].seq = i / NBUF; __threadfence_block(); vstore(&hdr[b].state, BUF_QUIT); }
+        __syncwarp();
+        break;
+      }
       uint64_t first = 0;
       uint32_t n = 0;
       if constexpr (App::kWindow) {
@@ -73,6 +84,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
         hdr[b].total = n ? buf_pre(b)[n] : 0;
         hdr[b].next = 0;
         hdr[b].left = 0;
+        hdr[b].seq = i / NBUF;
         __threadfence_block();
         vstore(&hdr[b].state, n ? BUF_READY : BUF_QUIT);
       }
@@ -84,9 +96,15 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
     RingSink sink{q};
     uint32_t pushed = 0;
     uint64_t edges = 0;
-    for (int b = 0;; b = (b + 1) % NBUF) {
-      int s;
-      for (unsigned ns = 8; (s = vload(&hdr[b].state)) == BUF_FREE; ns = ns < 128 ? ns * 2 : ns) __nanosleep(ns);
+    for (int i = 0;; ++i) {
+      const int b = i % NBUF, pass = i / NBUF;
+      int s = BUF_FREE;
+      for (unsigned ns = 8;; ns = ns < 128 ? ns * 2 : ns) {
+        s = vload(&hdr[b].state);
+        if (s != BUF_FREE && vload(&hdr[b].seq) == pass) break;
+        __nanosleep(ns);
+        if (ns >= 128 && (q_aborted(q) || q_timed_out(q))) { s = BUF_QUIT; break; }
+      }
       if (s == BUF_QUIT) break;
       __threadfence_block();
       const int n = hdr[b].n;
