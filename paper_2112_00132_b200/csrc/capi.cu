@@ -247,6 +247,7 @@ static void graph_free(atos_graph g) {
   cudaFree(w.ctl);
   cudaFree(w.u32a);
   cudaFree(w.u32b);
+  cudaFree(w.u16a);
   cudaFree(w.f32a);
   cudaFree(w.f32b);
   cudaFree(w.f64a);
@@ -601,18 +602,19 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
   CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)n, !bsp, c.s));
   CKS(ensure(w.u32a, w.u32a_n, (size_t)n));
   CKS(ensure(w.u32b, w.u32b_n, (size_t)n));
+  CKS(ensure(w.u16a, w.u16a_n, (size_t)n));
   if (bsp) {
     CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
     CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
   }
   CK(cudaEventRecord(w.ev[0], c.s));
   // a2: init (timed)
-  k_bfs_init<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, w.u32b, n, src);
+  k_bfs_init<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, w.u32b, w.u16a, n, src);
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : 1, w.ring, bsp ? -1 : src);
   CK(cudaGetLastError());
   c.launches += 2;
   CK(cudaEventRecord(w.ev[1], c.s));
-  BfsApp app{w.u32a, w.u32b, c.cfg.bfs_filter};
+  BfsApp app{w.u32a, w.u32b, w.u16a, c.cfg.bfs_filter};
   using P = EdgeMapPolicy<BfsApp>;
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
     CKS(run_persistent<P>(c, app, make_queue(g, c.cfg, 0)));

@@ -17,6 +17,8 @@ struct Workspace {
   size_t u32a_n = 0;
   uint32_t* u32b = nullptr;         // BFS done (expanded-at-depth)
   size_t u32b_n = 0;
+  uint16_t* u16a = nullptr;         // BFS near (2-byte dist mirror for the edge filter)
+  size_t u16a_n = 0;
   float* f32a = nullptr;  // PR rank / GC colour
   size_t f32a_n = 0;
   float* f32b = nullptr;  // PR residue

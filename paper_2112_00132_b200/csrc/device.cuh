@@ -167,6 +167,14 @@ __device__ __forceinline__ uint32_t ld_probe_hot(const uint32_t* p) {  // cta sc
   asm volatile("ld.relaxed.cta.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_last()));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_probe_u16(const uint16_t* p) {  // cta scope, L1-cacheable, evict_last
+  uint16_t v;
+  asm volatile("ld.relaxed.cta.global.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol_evict_last()));
+  return v;
+}
+__device__ __forceinline__ void st_u16_hot(uint16_t* p, uint16_t v) {
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(p), "h"(v), "l"(pol_evict_last()));
+}
 __device__ __forceinline__ uint32_t ld_relaxed_hot(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_last()));

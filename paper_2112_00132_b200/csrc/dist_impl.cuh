@@ -360,7 +360,8 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
     CKS(ensure(w.u32b, w.u32b_n, (size_t)std::max<int64_t>(n, 1)));
     if (!d->sent_min) CK(cudaMalloc(&d->sent_min, (size_t)N * sizeof(uint32_t)));
     const bool mine = src >= g->v_begin && src < g->v_end;
-    k_bfs_init<<<fill_blocks(std::max<int64_t>(n, 1), g->sms), 256, 0, c.s>>>(w.u32a, w.u32b, n, mine ? src - g->v_begin : -1);
+    k_bfs_init<<<fill_blocks(std::max<int64_t>(n, 1), g->sms), 256, 0, c.s>>>(w.u32a, w.u32b, nullptr, n,
+                                                                               mine ? src - g->v_begin : -1);
     k_fill<uint32_t><<<fill_blocks(N, g->sms), 256, 0, c.s>>>(d->sent_min, N, 0xFFFFFFFFu);
     k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, mine ? 1 : 0, w.ring, mine ? src - g->v_begin : -1);
     d->launches += 3;

@@ -38,6 +38,11 @@ struct BfsApp {
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   uint32_t* dist;
   uint32_t* done;  // done[v] = smallest depth at which v has been expanded (init MAX)
+  // near[v] = min(dist[v], 0xFFFF) as of some moment (stale values are larger,
+  // never smaller): a 2-byte mirror of dist that the per-edge filter probes.
+  // At 32 MB (RMAT-24) it stays L2-resident where the 64 MB dist array
+  // missed 38% of probes into random DRAM sectors (profiles/r01_bfs_*).
+  uint16_t* near;
   int filter;
   using Payload = uint32_t;
   using Probe = uint32_t;
@@ -48,7 +53,11 @@ struct BfsApp {
   // any atomic (memory-level parallelism).  The probe may hit a stale L1 copy
   // (>= the current value): it only lets through atomics that turn out not to
   // improve, never suppresses one that would.
-  __device__ __forceinline__ Probe probe(uint32_t w) const { return filter ? ld_probe_hot(dist + w) : 0xFFFFFFFFu; }
+  __device__ __forceinline__ Probe probe(uint32_t w) const {
+    if (!filter) return 0xFFFFFFFFu;
+    const uint32_t v = ld_probe_u16(near + w);
+    return v == 0xFFFFu ? 0xFFFFFFFFu : v;
+  }
   __device__ __forceinline__ bool commit(Payload nd, uint32_t w, Probe pr) const {
     return decide(nd, w, pr, issue(nd, w, pr));
   }
@@ -58,7 +67,11 @@ struct BfsApp {
   __device__ __forceinline__ Raw issue(Payload nd, uint32_t w, Probe pr) const {
     return nd < pr ? atom_min_hot(dist + w, nd) : 0u;
   }
-  __device__ __forceinline__ bool decide(Payload nd, uint32_t, Probe pr, Raw old) const { return nd < pr && nd < old; }
+  __device__ __forceinline__ bool decide(Payload nd, uint32_t w, Probe pr, Raw old) const {
+    const bool improved = nd < pr && nd < old;
+    if (improved) st_u16_hot(near + w, nd < 0xFFFFu ? (uint16_t)nd : (uint16_t)0xFFFFu);
+    return improved;
+  }
   // Expand v at its CURRENT depth d (R3) unless some task already expanded
   // (or is expanding) v at depth <= d: a vertex pushed k times by k
   // improvements is expanded at most once per distinct depth it is popped at.
@@ -87,8 +100,8 @@ struct BfsApp {
     return atomicMin(done + v, x.d) > x.d;
   }
   __device__ __forceinline__ bool edge(Payload nd, uint32_t w) const {
-    if (filter && nd >= ld_relaxed_u32(dist + w)) return false;
-    return nd < atom_min_hot(dist + w, nd);
+    const Probe pr = probe(w);
+    return decide(nd, w, pr, issue(nd, w, pr));
   }
 };
 
