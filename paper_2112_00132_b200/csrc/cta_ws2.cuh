@@ -17,6 +17,8 @@
 namespace atos {
 
 constexpr int NBUF = 4;
+constexpr int STEP_CAP = 2048;  // per-buffer step-owner table (steps beyond it search)
+constexpr int64_t STEP_EDGES = 32 * LBS_UNROLL;
 enum : int { BUF_FREE = 0, BUF_READY = 1, BUF_QUIT = 2 };
 
 struct BufHdr {
@@ -29,8 +31,12 @@ struct BufHdr {
 };
 
 template <class Payload>
+__host__ __device__ constexpr size_t ws2_buf_bytes(int F) {
+  return ws_buf_bytes<Payload>(F) + (size_t)STEP_CAP * 4;
+}
+template <class Payload>
 __host__ __device__ constexpr size_t ws2_smem_bytes(int F) {
-  return (size_t)NBUF * ws_buf_bytes<Payload>(F) + NBUF * sizeof(BufHdr) + 64;
+  return (size_t)NBUF * ws2_buf_bytes<Payload>(F) + NBUF * sizeof(BufHdr) + 64;
 }
 
 __device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
@@ -41,8 +47,9 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
                                    LocalStats& st) {
   using Payload = typename App::Payload;
   const int T = blockDim.x, tid = threadIdx.x, wid = tid >> 5, lane = lane_id();
-  const size_t bb = ws_buf_bytes<Payload>(F);
+  const size_t bb = ws2_buf_bytes<Payload>(F);
   BufHdr* hdr = reinterpret_cast<BufHdr*>(smem + NBUF * bb);
+  auto buf_own = [&](int b) { return reinterpret_cast<int*>(smem + b * bb + ws_buf_bytes<Payload>(F)); };
   auto buf_e0 = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb); };
   auto buf_pre = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb) + F; };
   auto buf_pay = [&](int b) { return reinterpret_cast<Payload*>(reinterpret_cast<int64_t*>(smem + b * bb) + 2 * F + 1); };
@@ -77,7 +84,16 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       }
       if (n) {
         agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b));
-        warp_exclusive_scan(buf_pre(b), (int)n);
+        int64_t* pre = buf_pre(b);
+        warp_exclusive_scan(pre, (int)n);
+        // step-owner table: own[c] = item holding flattened edge c*STEP_EDGES
+        int* own = buf_own(b);
+        for (uint32_t it = lane; it < n; it += 32) {
+          const int64_t c0 = (pre[it] + STEP_EDGES - 1) / STEP_EDGES;
+          const int64_t c1 = min((pre[it + 1] + STEP_EDGES - 1) / STEP_EDGES, (int64_t)STEP_CAP);
+          for (int64_t c = c0; c < c1; ++c) own[c] = (int)it;
+        }
+        __syncwarp();
       }
       if (lane == 0) {
         hdr[b].n = (int)n;
@@ -112,13 +128,19 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       const int64_t* pre = buf_pre(b);
       const int64_t* e0 = buf_e0(b);
       const Payload* pay = buf_pay(b);
+      const int* own = buf_own(b);
       const int64_t steps = (total + 32 * LBS_UNROLL - 1) / (32 * LBS_UNROLL);
       for (;;) {
         int c = 0;
         if (lane == 0) c = atomicAdd(&hdr[b].next, 1);
         c = __shfl_sync(FULL_MASK, c, 0);
         if ((int64_t)c >= steps) break;
-        const uint32_t p = lbs_step(app, g, sink, pre, e0, pay, n, total, (int64_t)c * 32 * LBS_UNROLL);
+        int hlo = -1, hhi = -1;
+        if (c < STEP_CAP) {
+          hlo = own[c];
+          hhi = (c + 1 < steps && c + 1 < STEP_CAP) ? own[c + 1] : n - 1;
+        }
+        const uint32_t p = lbs_step(app, g, sink, pre, e0, pay, n, total, (int64_t)c * STEP_EDGES, hlo, hhi);
         if (lane == 0) pushed += p;
         if (lane == 0) edges += (uint64_t)min((int64_t)32 * LBS_UNROLL, total - (int64_t)c * 32 * LBS_UNROLL);
       }

@@ -472,17 +472,25 @@ struct SmemComb {
 
 // One LBS step: the warp expands flattened edges [eb, eb + 32*UNROLL) of a
 // prepared batch (see lbs_expand).  Returns the pushes (warp-uniform).
+// hint_lo/hint_hi (>= 0): owners of the step's first edge and of the first
+// edge of the next step, precomputed by the queue agent (no per-step search).
 template <class App, class Sink>
 __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
                                              const int64_t* e0s, const typename App::Payload* pay, int n,
-                                             int64_t total, int64_t eb) {
+                                             int64_t total, int64_t eb, int hint_lo = -1, int hint_hi = -1) {
   const int lane = lane_id();
-  const int64_t elast = min(total, eb + 32 * LBS_UNROLL) - 1;
-  int bound = 0;
-  if (lane == 0) bound = lbs_find(pre, n, eb);
-  if (lane == 31) bound = lbs_find(pre, n, elast);
-  int lo = __shfl_sync(FULL_MASK, bound, 0);
-  const int hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
+  int lo, hi;
+  if (hint_lo >= 0) {
+    lo = hint_lo;
+    hi = hint_hi + 1;
+  } else {
+    const int64_t elast = min(total, eb + 32 * LBS_UNROLL) - 1;
+    int bound = 0;
+    if (lane == 0) bound = lbs_find(pre, n, eb);
+    if (lane == 31) bound = lbs_find(pre, n, elast);
+    lo = __shfl_sync(FULL_MASK, bound, 0);
+    hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
+  }
   uint32_t w[LBS_UNROLL];
   int idx[LBS_UNROLL];
 #pragma unroll
