@@ -94,7 +94,7 @@ __device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g
         const uint32_t want = 2u * (uint32_t)(p >> q.log2cap) + 1u;
         if ((uint32_t)(raw[k] >> 32) == want) {
           it[k] = (uint32_t)raw[k];
-          st_relaxed_u64(q.ring + (p & q.mask), (uint64_t)(want + 1u) << 32);
+          st_stream_u64(q.ring + (p & q.mask), (uint64_t)(want + 1u) << 32);
         } else if (!q_load_slot(q, p, it[k])) {
           it[k] = 0xFFFFFFFFu;
         }

@@ -180,10 +180,17 @@ __device__ __forceinline__ uint32_t ld_relaxed_hot(const uint32_t* p) {
   asm volatile("ld.relaxed.gpu.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_last()));
   return v;
 }
-__device__ __forceinline__ int64_t ld_nc_s64(const int64_t* p) {
+__device__ __forceinline__ int64_t ld_nc_s64(const int64_t* p) {  // CSR offsets: read-only, evict_first
   int64_t v;
-  asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol_evict_first()));
   return v;
+}
+__device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {  // queue slot writes
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol_evict_first()) : "memory");
+}
+// per-pop accumulation into a large array (PR rank): keep it from evicting the residues
+__device__ __forceinline__ void red_add_cold(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol_evict_first()));
 }
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
@@ -344,7 +351,9 @@ __device__ __forceinline__ bool q_load_slot(const Queue& q, uint64_t p, uint32_t
     }
   }
   item = (uint32_t)w;
-  st_relaxed_u64(slot, (uint64_t)(2u * lap + 2u) << 32);
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(slot), "l"((uint64_t)(2u * lap + 2u) << 32),
+               "l"(pol_evict_first())
+               : "memory");
   return true;
 }
 

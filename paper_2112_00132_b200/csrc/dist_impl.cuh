@@ -123,7 +123,7 @@ struct PrPartAppT {
   }
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
     if (x.r == R(0)) return false;
-    atomicAdd(rank + v, (double)x.r);
+    red_add_cold(rank + v, (double)x.r);
     if (x.e1 == x.e0) return false;
     p = alpha * x.r / (R)(x.e1 - x.e0);
     return true;

@@ -150,7 +150,7 @@ struct PrAppT {
   }
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
     if (x.r == R(0)) return false;
-    atomicAdd(rank + v, (double)x.r);
+    red_add_cold(rank + v, (double)x.r);
     if (x.e1 == x.e0) return false;
     p = alpha * x.r / (R)(x.e1 - x.e0);
     return true;
@@ -208,7 +208,7 @@ struct PrWindowAppT {
   }
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
     if (x.r == R(0)) return false;
-    atomicAdd(rank + v, (double)x.r);
+    red_add_cold(rank + v, (double)x.r);
     if (x.e1 == x.e0) return false;
     p = alpha * x.r / (R)(x.e1 - x.e0);
     return true;

@@ -30,7 +30,43 @@ __global__ void k(float* a, uint32_t* u, uint32_t mask, uint64_t ops_per_thread,
   }
   if (acc == 12345.f) *sink = acc;
 }
+__global__ void krand_big(const float* a, uint64_t mask, uint64_t ops_per_thread, float* sink) {
+  uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  float acc = 0;
+  for (uint64_t i = 0; i < ops_per_thread; i += 8) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint64_t h = hash32(tid * 0x9E3779B9u + (uint32_t)(i + j) * 0x85EBCA6Bu);
+      h = (h << 32) | hash32((uint32_t)h ^ 0x1234567u);
+      v[j] = __ldcg(a + ((h & mask) << 3));  // one float per 32-byte sector
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += v[j];
+  }
+  if (acc == 12345.f) *sink = acc;
+}
+
 int main() {
+  {
+    // random 32-byte sectors over 4 GB (L2 misses): DRAM random-access rate
+    const uint64_t bytes = 4ull << 30;
+    float* big; float* s0;
+    cudaMalloc(&big, bytes); cudaMalloc(&s0, 4); cudaMemset(big, 0, bytes);
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const uint64_t sectors = bytes / 32;
+    int blocks = sms * 8, threads = 256; uint64_t opt = 512;
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      krand_big<<<blocks, threads>>>(big, sectors - 1, opt, s0);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+    }
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double ops = (double)blocks * threads * opt;
+    printf("%-34s           %8.1f G sectors/s = %7.1f GB/s of 32-B sectors (%.2f ms)\n", "random sector loads over 4 GB", ops / ms / 1e6, ops * 32 / ms / 1e6, ms);
+    cudaFree(big);
+  }
   const uint32_t n = 1u << 24;
   float* a; uint32_t* u; float* s;
   cudaMalloc(&a, n * 4); cudaMalloc(&u, n * 4); cudaMalloc(&s, 4);
