@@ -67,7 +67,7 @@ __device__ __forceinline__ void warp_exclusive_scan(int64_t* a, int n) {
 // at a time in phases — slot loads, then every item's begin loads, then every
 // item's begin atomics — so ~3 L2 round trips cover 32*AGENT_G items instead
 // of ~3 per item (the agent warp was the bottleneck on low-degree frontiers).
-constexpr int AGENT_G = 8;
+constexpr int AGENT_G = 4;
 
 template <class App>
 __device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g, const Queue& q, const Queue* cq,

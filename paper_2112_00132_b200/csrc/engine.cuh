@@ -397,7 +397,7 @@ __device__ __forceinline__ int lbs_find_range(const int64_t* pre, int lo, int hi
   return lo;
 }
 
-constexpr int LBS_UNROLL = 4;
+constexpr int LBS_UNROLL = 8;
 
 // Hub splitting (persistent CTA workers): a popped vertex with more than
 // SPLIT_DEG edges keeps its first CHUNK_EDGES edges and publishes the rest as
