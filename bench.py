@@ -48,9 +48,10 @@ def parse():
     ap.add_argument("--impl", default="atos", choices=["atos", "reference"])
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=16)
-    ap.add_argument("--fetch", type=int, default=256)
-    ap.add_argument("--threads", type=int, default=256)
-    ap.add_argument("--pr-fetch", type=int, default=256)
+    ap.add_argument("--fetch", type=int, default=128, help="BFS FETCH_SIZE")
+    ap.add_argument("--threads", type=int, default=256, help="BFS cta_threads")
+    ap.add_argument("--pr-fetch", type=int, default=128, help="PageRank FETCH_SIZE")
+    ap.add_argument("--pr-threads", type=int, default=512, help="PageRank cta_threads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-kernel-bfs", default="persistent", choices=["persistent", "discrete"],
@@ -190,7 +191,7 @@ def run_atos(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     cfg_bfs = atos.Config(kernel="persistent", worker="cta", fetch_size=args.fetch, cta_threads=args.threads,
                           timeout_s=120)
-    cfg_pr = atos.Config(kernel="persistent", worker="cta", fetch_size=args.pr_fetch, cta_threads=args.threads,
+    cfg_pr = atos.Config(kernel="persistent", worker="cta", fetch_size=args.pr_fetch, cta_threads=args.pr_threads,
                          timeout_s=120)
     G = atos.Graph(g.off, g.col)
     depth = torch.empty(g.n, dtype=torch.int32, device=dev)
@@ -254,6 +255,7 @@ def run_atos(args, rank, world, local_rank):
         "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_bfs0+pagerank", "scale": args.scale,
                    "edge_factor": args.edge_factor, "n": g.n, "m": g.m, "kernel": "persistent", "worker": "cta",
                    "fetch_size": args.fetch, "pr_fetch_size": args.pr_fetch, "cta_threads": args.threads,
+                   "pr_cta_threads": args.pr_threads,
                    "alpha": ALPHA, "eps": EPS, "l2": "flushed (512 MB write) between steps; inputs 1.2 GB > L2",
                    "parallelism": "replicas" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": pr_ach, "peak": hbm, "unit": "GB/s", "frac": pr_ach / hbm,
