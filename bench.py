@@ -121,6 +121,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def ncu_traffic(key):
+    """Per-launch DRAM traffic of a kernel from the committed ncu capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f)[key]["bytes"]
+    except Exception:
+        return None
+
+
 def make_graph(args):
     import graphgen as gg
     t = time.time()
@@ -259,7 +268,9 @@ def run_atos(args, rank, world, local_rank):
                    "alpha": ALPHA, "eps": EPS, "l2": "flushed (512 MB write) between steps; inputs 1.2 GB > L2",
                    "parallelism": "replicas" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": pr_ach, "peak": hbm, "unit": "GB/s", "frac": pr_ach / hbm,
-                     "traffic": None, "kernel": "k_persistent<PrAppT<float>, CTA>",
+                     "traffic": ncu_traffic("pagerank_persistent_cta"),
+                     "traffic_source": "profiles/r01_traffic.json (ncu --set full, same config)",
+                     "algorithmic_bytes": pr_bytes, "kernel": "k_persistent<PrAppT<float>, CTA>",
                      "bytes_model": "8 B/edge push + 32 B/pop", "peak_kind": peak_kind},
         "bfs": {"gteps": e_bfs / (statistics.mean(t_bfs) * 1e-3) / 1e9, "ms": statistics.mean(t_bfs),
                 "kernel_ms": bfs_kms, "edges": e_bfs, "reached": v_bfs,
