@@ -1,0 +1,144 @@
+"""Round experiments (configs of BASELINE.json beyond the bench line), markdown to stdout.
+
+  heatmap   BFS worker size x FETCH_SIZE sweep on the 4899x4899 grid (configs[3]; the
+            paper's fig:heatmap analog) and on RMAT-20
+  kernels   persistent vs discrete vs BSP on RMAT-24 for BFS and PageRank (configs[2])
+  color     greedy colouring on RMAT-16 (configs[1]): time-to-colour, colours vs the
+            oracle, overwork; permuted vs unpermuted ids; all kernels/workers
+  grid      BFS on the 24M-vertex grid and the road-like variant: ms, per-hop latency
+  timeline  cumulative work vs time for BFS/PR on RMAT-24
+"""
+import os
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import graphgen as gg  # noqa: E402
+import paper_2112_00132_b200 as atos  # noqa: E402
+
+
+def timed(fn, reps=3):
+    out = [fn() for _ in range(reps)]
+    return out[-1], statistics.median(o[1]["ms"] for o in out)
+
+
+def heatmap():
+    sizes = [(8, "thread", 256), (32, "warp", 256), (64, "cta", 64), (128, "cta", 128), (256, "cta", 256),
+             (512, "cta", 512), (1024, "cta", 1024)]
+    fetches = [1, 4, 16, 64, 256, 1024]
+    for gname, g in [("grid 4899x4899 (24.0M vertices, 96.0M arcs, ecc. 9,796)", gg.grid(4899, 4899)),
+                     ("RMAT-20 (1.05M vertices, 16.1M arcs)", gg.rmat(20, 16, seed=1))]:
+        G = atos.Graph.from_csr(g)
+        print(f"\n### BFS from 0 on {gname}: ms (overwork = pops / reached)\n")
+        print("| worker (threads) | " + " | ".join(f"F={f}" for f in fetches) + " |")
+        print("|---|" + "---|" * len(fetches))
+        for _, w, t in sizes:
+            row = []
+            for f in fetches:
+                try:
+                    (d, st), ms = timed(lambda: atos.bfs(G, 0, worker=w, cta_threads=t, fetch_size=f, timeout_s=120), 2)
+                    reached = int(np.sum(d != atos.UNREACHED))
+                    row.append(f"{ms:.2f} ({st['tasks_popped'] / reached:.2f})")
+                except atos.AtosError as e:
+                    row.append(e.name)
+            label = f"{w} ({t})"
+            print(f"| {label} | " + " | ".join(row) + " |", flush=True)
+        del G
+
+
+def kernels():
+    g = gg.rmat(24, 16, seed=1)
+    G = atos.Graph.from_csr(g)
+    deg = g.degrees()
+    print("\n### RMAT-24: persistent vs discrete vs BSP (CTA workers)\n")
+    print("| app | kernel | ms | launches | rounds | pops | edges | GTEPS |")
+    print("|---|---|---|---|---|---|---|---|")
+    for kern in ["persistent", "discrete", "bsp"]:
+        (d, st), ms = timed(lambda: atos.bfs(G, 0, kernel=kern, fetch_size=128, timeout_s=300), 3)
+        e = int(deg[d != atos.UNREACHED].sum())
+        print(f"| BFS | {kern} | {ms:.2f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
+              f"{st['edges_processed']} | {e / ms / 1e6:.1f} |", flush=True)
+    for kern in ["persistent", "discrete", "bsp"]:
+        (r, st), ms = timed(lambda: atos.pagerank(G, 0.85, 1e-6, kernel=kern, fetch_size=128, cta_threads=512,
+                                                  timeout_s=300), 1)
+        print(f"| PageRank | {kern} | {ms:.1f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
+              f"{st['edges_processed']} | {st['edges_processed'] / ms / 1e6:.1f} (raw) |", flush=True)
+    (r, st), ms = timed(lambda: atos.pagerank(G, 0.85, 1e-6, pr_activation=1, check_size=8, fetch_size=128,
+                                              cta_threads=512, timeout_s=300), 1)
+    print(f"| PageRank (Check_Size=8 window, f1) | persistent | {ms:.1f} | {st['kernel_launches']} | {st['rounds']} | "
+          f"{st['tasks_popped']} | {st['edges_processed']} | {st['edges_processed'] / ms / 1e6:.1f} (raw) |", flush=True)
+
+
+def color():
+    import oracle
+    print("\n### Colouring: time-to-colour, colours (GPU vs serial first-fit oracle), overwork = tasks / 2n\n")
+    print("| graph | kernel | worker | ms | colours | oracle colours | overwork |")
+    print("|---|---|---|---|---|---|---|")
+    for gname, g in [("RMAT-16 sym", gg.rmat(16, 16, seed=1, symmetrize=True)),
+                     ("RMAT-16 sym, permuted ids", gg.rmat(16, 16, seed=1, symmetrize=True, perm_seed=7)),
+                     ("RMAT-22 sym", gg.rmat(22, 16, seed=1, symmetrize=True)),
+                     ("RMAT-22 sym, permuted ids", gg.rmat(22, 16, seed=1, symmetrize=True, perm_seed=7)),
+                     ("grid 1024x1024", gg.grid(1024, 1024))]:
+        G = atos.Graph.from_csr(g, symmetric=True)
+        _, k_or = oracle.greedy_color(g)
+        for kern, w in [("persistent", "warp"), ("persistent", "cta"), ("discrete", "warp"), ("discrete", "cta"),
+                        ("bsp", "cta")]:
+            (c, k, st), ms = timed(lambda: atos.color(G, kernel=kern, worker=w, fetch_size=32 if w == "warp" else 256,
+                                                      timeout_s=300), 3)
+            bad, _ = oracle.check_coloring(g, c)
+            assert bad == 0
+            print(f"| {gname} | {kern} | {w} | {ms:.2f} | {k} | {k_or} | {st['tasks_popped'] / (2 * g.n):.2f} |",
+                  flush=True)
+
+
+def grid():
+    print("\n### High-diameter BFS (configs[3])\n")
+    print("| graph | worker | F | ms | per-hop us | pops/reached |")
+    print("|---|---|---|---|---|---|")
+    for gname, g, ecc in [("grid 4899x4899", gg.grid(4899, 4899), 9796),
+                          ("road-like 4899x4899 (40% edges dropped)", gg.grid(4899, 4899, drop_prob=0.4, seed=3), None)]:
+        G = atos.Graph.from_csr(g)
+        for w, t, f in [("cta", 256, 128), ("cta", 64, 16), ("warp", 256, 4), ("thread", 256, 1)]:
+            (d, st), ms = timed(lambda: atos.bfs(G, 0, worker=w, cta_threads=t, fetch_size=f, timeout_s=300), 2)
+            reached = d != atos.UNREACHED
+            e = int(d[reached].max())
+            print(f"| {gname} | {w} ({t}) | {f} | {ms:.1f} | {ms * 1e3 / e:.2f} (ecc {e}) | "
+                  f"{st['tasks_popped'] / reached.sum():.3f} |", flush=True)
+
+
+def timeline():
+    g = gg.rmat(24, 16, seed=1)
+    G = atos.Graph.from_csr(g)
+    tr = atos.Trace(1 << 22)
+    for app in ["bfs", "pr"]:
+        if app == "bfs":
+            atos.bfs(G, 0, fetch_size=128)
+            _, st = atos.bfs(G, 0, fetch_size=128, trace=tr)
+        else:
+            _, st = atos.pagerank(G, 0.85, 1e-6, fetch_size=128, cta_threads=512, trace=tr)
+        r = tr.records(st)
+        t = (r["t_ns"] - r["t_ns"][0]) / 1e3
+        nb = 20
+        edges = np.linspace(0, t[-1] + 1e-9, nb + 1)
+        idx = np.clip(np.searchsorted(edges, t, side="right") - 1, 0, nb - 1)
+        tot = r["edges"].astype(np.int64).sum()
+        print(f"\n### Timeline: {app.upper()} RMAT-24 ({st['ms']:.2f} ms, {len(r)} batches)\n")
+        print("| t (us) | batches | items | edges | cum. edges % | SMs active |")
+        print("|---|---|---|---|---|---|")
+        cum = 0
+        for b in range(nb):
+            m = idx == b
+            eb = int(r["edges"][m].astype(np.int64).sum())
+            cum += eb
+            print(f"| {edges[b]:.0f} | {int(m.sum())} | {int(r['items'][m].sum())} | {eb} | {100 * cum / tot:.1f} | "
+                  f"{len(np.unique(r['sm'][m]))} |")
+
+
+if __name__ == "__main__":
+    for name in sys.argv[1:]:
+        t0 = time.time()
+        globals()[name]()
+        print(f"\n_({name}: {time.time() - t0:.0f} s)_", flush=True)
