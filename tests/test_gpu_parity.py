@@ -123,6 +123,45 @@ def test_bfs_serial_order_identity(atos):
         assert st["tasks_popped"] == int(np.sum(exp != oracle.UNREACHED)), name
 
 
+def test_bfs_deep_path_beyond_u16_mirror(atos):
+    """Depths above 65,534 saturate the 2-byte dist mirror used by the edge
+    filter; the filter must then defer to the 32-bit atomicMin (R25 notes)."""
+    g = gg.path(70000)
+    for cfg in [dict(), dict(worker="warp", fetch_size=4), dict(kernel="bsp")]:
+        d, _ = atos.bfs(atos.Graph.from_csr(g), 0, **cfg)
+        assert np.array_equal(d, np.arange(70000, dtype=np.uint32)), cfg
+
+
+def test_trace_records(atos):
+    g = G("rmat16")
+    tr = atos.Trace(1 << 16)
+    d, st = atos.bfs(D(atos, "rmat16"), 0, trace=tr)
+    r = tr.records(st)
+    assert st["trace_records"] == len(r) > 0
+    assert np.all(np.diff(r["t_ns"].astype(np.int64)) >= 0)
+    # every popped task is in exactly one record (chunk tasks included)
+    assert int(r["items"].sum()) == st["tasks_popped"] + st["chunk_tasks"]
+    assert int(r["edges"].astype(np.int64).sum()) == st["edges_processed"]
+    assert set(np.unique(r["kind"]).tolist()) == {0}
+
+
+def test_stats_invariants(atos):
+    g = G("rmat16")
+    exp = oracle.bfs(g, 0)
+    reach = exp != oracle.UNREACHED
+    for cfg in [dict(), dict(worker="warp"), dict(worker="thread", fetch_size=1), dict(kernel="discrete"),
+                dict(kernel="bsp")]:
+        d, st = atos.bfs(D(atos, "rmat16"), 0, **cfg)
+        assert st["tasks_pushed"] == st["tasks_popped"] - 1 or cfg.get("kernel") == "bsp", cfg  # src + pushes
+        assert st["edges_processed"] >= int(g.degrees()[reach].sum()), cfg
+        assert st["kernel_launches"] >= 1 and st["ms"] > 0
+
+
+def test_bfs_adaptive_fetch_off(atos):
+    d, st = atos.bfs(D(atos, "rmat16"), 0, adaptive_fetch=False)
+    assert np.array_equal(d, oracle.bfs(G("rmat16"), 0))
+
+
 def test_bfs_device_output_and_torch_borrow(atos):
     import torch
     g = G("rmat12")
