@@ -179,7 +179,7 @@ __device__ __forceinline__ uint32_t window_pop(const App& app, const Queue& q, u
         state = 2;
       } else {
         const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
-        t0 = ld_relaxed_u64(&q.ctl->tail.v);
+        t0 = q_enqueued(q);
         if (p == t0 && atomicCAS(reinterpret_cast<unsigned long long*>(&q.ctl->aux[3].v), 0ull, 1ull) == 0ull) state = 1;
       }
     }
@@ -200,7 +200,7 @@ __device__ __forceinline__ uint32_t window_pop(const App& app, const Queue& q, u
       if (lane_id() == 0) {
         __threadfence();
         const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
-        const uint64_t t = ld_relaxed_u64(&q.ctl->tail.v);
+        const uint64_t t = q_enqueued(q);
         done = found == 0 && p == t && t == t0;
         st_relaxed_u64(&q.ctl->aux[3].v, done ? 2ull : 0ull);
       }

@@ -22,7 +22,8 @@ constexpr int NBUF = 4;
 // shared memory and the CTA's agent takes them next, skipping the global
 // push -> poll -> pop round trip on the critical path of high-diameter
 // graphs (9.5 us per hop on the 4899^2 grid without it).  Kept items are
-// counted in `tail` (atomicAdd) so termination (a7) is unchanged.
+// counted in ctl->kept (they take no ring position), and quiescence (a7) is
+// processed == tail + kept.
 constexpr int LCAP = 128;  // per worker warp
 constexpr int STEP_CAP = 2048;  // per-buffer step-owner table (steps beyond it search)
 constexpr int64_t STEP_EDGES = 32 * LBS_UNROLL;
@@ -69,8 +70,8 @@ struct KeepSink {
     const int t = *(volatile const int*)tail;
     const bool local = *(volatile const int*)keep && (int)total <= LCAP - (t - *(volatile const int*)head);
     if (!local) return q_warp_push_multi<U>(q, pred, item);
-    if (lane_id() == 0)  // count the kept items as pushed (termination); wait for it to be performed
-      (void)atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)total);
+    if (lane_id() == 0)  // count the kept items as enqueued (termination); wait for it to be performed
+      (void)atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->kept.v), (unsigned long long)total);
     const unsigned lt = lanemask_lt();
     int base = t;
 #pragma unroll
@@ -144,7 +145,7 @@ __device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uin
           if (qlen > hw) hw = qlen;
         } else {
           const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
-          const uint64_t t = ld_relaxed_u64(&q.ctl->tail.v);
+          const uint64_t t = q_enqueued(q);
           quit = p == t;
         }
       }

@@ -221,6 +221,7 @@ struct QueueCtl {
   Line64 chunk_tail;    // hub chunk table: entries allocated
   Line64 chunk_done;    // hub chunk table: entries consumed
   Line64 trace_count;   // timeline records produced
+  Line64 kept;          // tasks kept in CTA-local continuation rings (no ring position)
   Line64 stats[4];      // popped, pushed, edges, spare
   Line64 aux[4];        // app-specific counters (e.g. PR check cursor, colours)
 };
@@ -465,6 +466,13 @@ __device__ __forceinline__ uint32_t q_try_pop(const Queue& q, uint32_t want, uin
   return n;
 }
 
+// Tasks ever enqueued = ring positions handed out (tail) + tasks kept in
+// CTA-local rings.  Read AFTER `processed`: processed <= enqueued always, so
+// equality at the reads implies equality (quiescence) at the processed read.
+__device__ __forceinline__ uint64_t q_enqueued(const Queue& q) {
+  return ld_relaxed_u64(&q.ctl->tail.v) + ld_relaxed_u64(&q.ctl->kept.v);
+}
+
 // Leader-side pop with the idle path (the paper's f2 hook): backoff,
 // termination poll (a7) and watchdog.  Returns n > 0 with `first`, or 0 when
 // the run is over (quiescent or aborted).
@@ -480,7 +488,7 @@ __device__ __forceinline__ uint32_t q_pop_or_quit(const Queue& q, uint32_t want,
     }
     // f2: failed pop.  Quiescence: processed (acquire) read BEFORE tail.
     const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
-    const uint64_t t = ld_relaxed_u64(&q.ctl->tail.v);
+    const uint64_t t = q_enqueued(q);
     if (p == t) return 0;
     if (q_aborted(q) || q_timed_out(q)) return 0;
     if (ns) __nanosleep(ns);

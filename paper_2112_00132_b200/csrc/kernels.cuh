@@ -304,6 +304,7 @@ __global__ void k_ctl_init(QueueCtl* ctl, uint64_t tail, uint64_t* ring, int64_t
   ctl->chunk_tail.v = 0;
   ctl->chunk_done.v = 0;
   ctl->trace_count.v = 0;
+  ctl->kept.v = 0;
   for (int i = 0; i < 4; ++i) { ctl->stats[i].v = 0; ctl->aux[i].v = 0; }
   if (src_item >= 0) ring[0] = (1ull << 32) | (uint64_t)(uint32_t)src_item;
 }
