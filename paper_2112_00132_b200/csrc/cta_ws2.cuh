@@ -97,7 +97,7 @@ __device__ __forceinline__ void vstore(int* p, int v) { *(volatile int*)p = v; }
 // the `keep` flag (global queue short => workers keep their activations).
 __device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& hw, int nw,
                                               const uint32_t* lrings, int* lhead, const int* ltail, int* keep,
-                                              uint32_t* gather, bool& from_local) {
+                                              uint32_t* gather, bool& from_local, bool allow_keep) {
   const int lane = lane_id();
   unsigned ns = 0;
   for (;;) {
@@ -140,7 +140,7 @@ __device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uin
       } else {
         n = q_try_pop(q, want, first, qlen);
         const long long cnt = (long long)ld_relaxed_u64(&q.ctl->count.v);
-        *(volatile int*)keep = cnt < (long long)q.workers * 2 ? 1 : 0;
+        *(volatile int*)keep = (allow_keep && cnt < (long long)q.workers * 2) ? 1 : 0;
         if (n) {
           if (qlen > hw) hw = qlen;
         } else {
@@ -203,7 +203,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       if constexpr (App::kWindow) {
         n = window_pop(app, q, (uint32_t)F, first, st.hw);
       } else {
-        n = agent_pop(q, (uint32_t)F, first, st.hw, nw, lrings, lhead, ltail, keep, gather, from_local);
+        n = agent_pop(q, (uint32_t)F, first, st.hw, nw, lrings, lhead, ltail, keep, gather, from_local, App::kKeep);
       }
       if (n) {
         agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b), from_local ? gather : nullptr);

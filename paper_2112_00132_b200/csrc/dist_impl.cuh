@@ -36,6 +36,8 @@ struct Outbox {
 // BFS on a partition: dist/done are local; sent_min (global n) filters remote
 // sends so a remote vertex is sent once per improvement of its tentative depth.
 struct BfsPartApp {
+  // CTA-local continuation while the global queue is short (BFS: latency; PR: more pops, off)
+  static constexpr bool kKeep = true;
   static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   uint32_t* dist;
@@ -97,6 +99,7 @@ struct BfsPartApp {
 // (global n, fp32) and are flushed as messages at the end of every round.
 template <class R>
 struct PrPartAppT {
+  static constexpr bool kKeep = false;
   static constexpr bool kCombine = true;
   static constexpr bool kWindow = false;
   double* rank;
@@ -150,6 +153,7 @@ struct PrPartAppT {
 // PR residue seeding on a partition (R4): local targets add to res, remote to racc.
 template <class R>
 struct PrPartInitAppT {
+  static constexpr bool kKeep = false;
   static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   R* res;

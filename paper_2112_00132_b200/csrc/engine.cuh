@@ -33,6 +33,8 @@ struct GraphView {
 // per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
 // (strict, R2).
 struct BfsApp {
+  // CTA-local continuation while the global queue is short (BFS: latency; PR: more pops, off)
+  static constexpr bool kKeep = true;
   static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
@@ -122,6 +124,7 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 
 template <class R>
 struct PrAppT {
+  static constexpr bool kKeep = false;
   static constexpr bool kCombine = true;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
@@ -181,6 +184,7 @@ struct PrAppT {
 // last completed task — a clean full sweep over unchanging residues.
 template <class R>
 struct PrWindowAppT {
+  static constexpr bool kKeep = false;
   static constexpr bool kCombine = false;
   static constexpr bool kWindow = true;
   double* rank;
@@ -234,6 +238,7 @@ struct PrWindowAppT {
 // but the frontier is rebuilt by the filter kernel, so nothing is appended.
 template <class R>
 struct PrBspAppT {
+  static constexpr bool kKeep = false;
   static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
