@@ -36,8 +36,7 @@ struct Outbox {
 // BFS on a partition: dist/done are local; sent_min (global n) filters remote
 // sends so a remote vertex is sent once per improvement of its tentative depth.
 struct BfsPartApp {
-  // CTA-local continuation while the global queue is short (BFS: latency; PR: more pops, off)
-  static constexpr bool kKeep = true;
+  static constexpr bool kKeep = false;
   static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   uint32_t* dist;

@@ -33,8 +33,10 @@ struct GraphView {
 // per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
 // (strict, R2).
 struct BfsApp {
-  // CTA-local continuation while the global queue is short (BFS: latency; PR: more pops, off)
-  static constexpr bool kKeep = true;
+  // CTA-local continuation (cta_ws2.cuh) measured slower on the 4899^2 grid
+  // (169 vs 93 ms: kept items wait in the CTA's batch pipeline) and 6.8x
+  // overwork on the road-like grid, so it is off for every app.
+  static constexpr bool kKeep = false;
   static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
