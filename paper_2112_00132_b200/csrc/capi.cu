@@ -393,8 +393,8 @@ static atos_status set_smem(K kern, size_t smem) {
 // Warp/thread workers stage their claimed items in shared memory (4 B per item,
 // FETCH per warp worker, 32*FETCH per thread-worker warp); shrink the block so
 // the staging buffer fits in 227 KB.  CTA workers keep cta_threads.
-static int clamp_threads(int W, int F, int T) {
-  if (W == W_CTA) return T;
+static int clamp_threads(int W, int F, int T, bool ws = false) {
+  if (W == W_CTA) return ws ? std::min(T, CTA_MAX_THREADS) : T;
   const size_t per_warp = (W == W_WARP ? (size_t)F : 32 * (size_t)F) * 4;
   int max_warps = (int)((227 * 1024) / per_warp);
   if (max_warps < 1) max_warps = 1;
@@ -404,7 +404,7 @@ static int clamp_threads(int W, int F, int T) {
 template <class P, class App, int W>
 static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q) {
   auto kern = k_persistent<P, App, W>;
-  const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads);
+  const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads, P::kWarpSpecialised);
   Queue qq = q;
   if (W == W_CTA && P::kSplit) {
     Workspace& w = c.g->ws;

@@ -26,7 +26,24 @@ constexpr int NBUF = 4;
 // processed == tail + kept.
 constexpr int LCAP = 128;  // per worker warp
 constexpr int STEP_CAP = 2048;  // per-buffer step-owner table (steps beyond it search)
-constexpr int64_t STEP_EDGES = 32 * LBS_UNROLL;
+// Register budget vs occupancy of the persistent CTA kernel (build-time knobs).
+// Measured on RMAT-24 (PR kernel ms / BFS ms): 1024x1 bound (64 regs, some
+// spills) + unroll 8: 209 / 4.1 — best; 512x1 (128 regs) + unroll 16:
+// 259 / 6.9; 256x3 (85 regs) + unroll 8: 257 / 4.0; 512x1 + unroll 8: 228 / 6.1.
+// Occupancy beats per-warp memory-level parallelism here.
+#ifndef ATOS_CTA_MAX_THREADS
+#define ATOS_CTA_MAX_THREADS 1024
+#endif
+#ifndef ATOS_CTA_MIN_BLOCKS
+#define ATOS_CTA_MIN_BLOCKS 1
+#endif
+#ifndef ATOS_WS_UNROLL
+#define ATOS_WS_UNROLL 8
+#endif
+constexpr int CTA_MAX_THREADS = ATOS_CTA_MAX_THREADS;
+constexpr int CTA_MIN_BLOCKS = ATOS_CTA_MIN_BLOCKS;
+constexpr int WS_UNROLL = ATOS_WS_UNROLL;
+constexpr int64_t STEP_EDGES = 32 * WS_UNROLL;
 enum : int { BUF_FREE = 0, BUF_READY = 1, BUF_QUIT = 2 };
 
 struct BufHdr {
@@ -253,7 +270,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       const int64_t* e0 = buf_e0(b);
       const Payload* pay = buf_pay(b);
       const int* own = buf_own(b);
-      const int64_t steps = (total + 32 * LBS_UNROLL - 1) / (32 * LBS_UNROLL);
+      const int64_t steps = (total + STEP_EDGES - 1) / STEP_EDGES;
       for (;;) {
         int c = 0;
         if (lane == 0) c = atomicAdd(&hdr[b].next, 1);
@@ -264,9 +281,10 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
           hlo = own[c];
           hhi = (c + 1 < steps && c + 1 < STEP_CAP) ? own[c + 1] : n - 1;
         }
-        const uint32_t p = lbs_step(app, g, sink, pre, e0, pay, n, total, (int64_t)c * STEP_EDGES, hlo, hhi);
+        const uint32_t p = lbs_step<App, KeepSink, WS_UNROLL>(app, g, sink, pre, e0, pay, n, total,
+                                                               (int64_t)c * STEP_EDGES, hlo, hhi);
         if (lane == 0) pushed += p;
-        if (lane == 0) edges += (uint64_t)min((int64_t)32 * LBS_UNROLL, total - (int64_t)c * 32 * LBS_UNROLL);
+        if (lane == 0) edges += (uint64_t)min(STEP_EDGES, total - (int64_t)c * STEP_EDGES);
       }
       if constexpr (App::kWindow) {
         // Alg. 4 lines 11-14: each popped vertex checks a Check_Size window

@@ -481,7 +481,7 @@ struct SmemComb {
 // prepared batch (see lbs_expand).  Returns the pushes (warp-uniform).
 // hint_lo/hint_hi (>= 0): owners of the step's first edge and of the first
 // edge of the next step, precomputed by the queue agent (no per-step search).
-template <class App, class Sink>
+template <class App, class Sink, int U = LBS_UNROLL>
 __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
                                              const int64_t* e0s, const typename App::Payload* pay, int n,
                                              int64_t total, int64_t eb, int hint_lo = -1, int hint_hi = -1) {
@@ -491,17 +491,17 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
     lo = hint_lo;
     hi = hint_hi + 1;
   } else {
-    const int64_t elast = min(total, eb + 32 * LBS_UNROLL) - 1;
+    const int64_t elast = min(total, eb + 32 * U) - 1;
     int bound = 0;
     if (lane == 0) bound = lbs_find(pre, n, eb);
     if (lane == 31) bound = lbs_find(pre, n, elast);
     lo = __shfl_sync(FULL_MASK, bound, 0);
     hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
   }
-  uint32_t w[LBS_UNROLL];
-  int idx[LBS_UNROLL];
+  uint32_t w[U];
+  int idx[U];
 #pragma unroll
-  for (int k = 0; k < LBS_UNROLL; ++k) {
+  for (int k = 0; k < U; ++k) {
     const int64_t e = eb + lane + 32 * k;
     idx[k] = -1;
     w[k] = 0;
@@ -511,24 +511,24 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
       w[k] = (uint32_t)ld_stream_s32(g.col + e0s[lo] + (e - pre[lo]));
     }
   }
-  typename App::Probe pr[LBS_UNROLL];
+  typename App::Probe pr[U];
 #pragma unroll
-  for (int k = 0; k < LBS_UNROLL; ++k)
+  for (int k = 0; k < U; ++k)
     if (idx[k] >= 0) pr[k] = app.probe(w[k]);
-  typename App::Raw raw[LBS_UNROLL];
-  typename App::Payload pk[LBS_UNROLL];
+  typename App::Raw raw[U];
+  typename App::Payload pk[U];
 #pragma unroll
-  for (int k = 0; k < LBS_UNROLL; ++k) {
+  for (int k = 0; k < U; ++k) {
     pk[k] = idx[k] >= 0 ? pay[idx[k]] : typename App::Payload{};
     if (idx[k] >= 0) raw[k] = app.issue(pk[k], w[k], pr[k]);
   }
-  bool act[LBS_UNROLL];
+  bool act[U];
 #pragma unroll
-  for (int k = 0; k < LBS_UNROLL; ++k) act[k] = idx[k] >= 0 && app.decide(pk[k], w[k], pr[k], raw[k]);
-  uint32_t item[LBS_UNROLL];
+  for (int k = 0; k < U; ++k) act[k] = idx[k] >= 0 && app.decide(pk[k], w[k], pr[k], raw[k]);
+  uint32_t item[U];
 #pragma unroll
-  for (int k = 0; k < LBS_UNROLL; ++k) item[k] = app.item_of(w[k]);
-  return sink.template warp_push_multi<LBS_UNROLL>(act, item);
+  for (int k = 0; k < U; ++k) item[k] = app.item_of(w[k]);
+  return sink.template warp_push_multi<U>(act, item);
 }
 
 template <class App, class Sink, class Comb = NoComb>

@@ -124,7 +124,9 @@ __host__ __device__ inline size_t worker_smem_bytes(int W, int F, int T, bool pe
 
 // ------------------------------------------------------------ persistent
 template <class P, class App, int W>
-__global__ void __launch_bounds__(1024, 1) k_persistent(App app, GraphView g, Queue q0, int F) {
+__global__ void __launch_bounds__((W == W_CTA && P::kWarpSpecialised) ? CTA_MAX_THREADS : 1024,
+                                  (W == W_CTA && P::kWarpSpecialised) ? CTA_MIN_BLOCKS : 1)
+    k_persistent(App app, GraphView g, Queue q0, int F) {
   extern __shared__ __align__(16) unsigned char smem[];
   Queue q = q0;
   q_arm(q);
