@@ -71,6 +71,7 @@ typedef struct {
   int32_t gc_literal;     /* 1: paper-literal Alg. 6 (both endpoints recolour) — ablation only */
   int32_t pr_residue_fp64; /* 1: PageRank residues in fp64 (rank is always fp64-accumulated)   */
   int32_t adaptive_fetch; /* 1 (default): pop min(FETCH, ceil(queued / workers)) items         */
+  int32_t device_loop;    /* discrete kernel: 1 = rounds driven by a CUDA-graph WHILE node    */
   int64_t queue_capacity; /* ring slots; 0 = auto (power of two >= 2n); rounded up to pow2     */
   double timeout_s;       /* device watchdog deadline in seconds; 0 = none                    */
   void* stream;           /* cudaStream_t to run on; NULL = legacy default stream             */

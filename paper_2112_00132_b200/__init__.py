@@ -52,7 +52,7 @@ class CConfig(ctypes.Structure):
                 ("cta_threads", ctypes.c_int32), ("fetch_size", ctypes.c_int32), ("num_blocks", ctypes.c_int32),
                 ("bfs_filter", ctypes.c_int32), ("pr_activation", ctypes.c_int32), ("check_size", ctypes.c_int32),
                 ("gc_literal", ctypes.c_int32), ("pr_residue_fp64", ctypes.c_int32),
-                ("adaptive_fetch", ctypes.c_int32),
+                ("adaptive_fetch", ctypes.c_int32), ("device_loop", ctypes.c_int32),
                 ("queue_capacity", ctypes.c_int64), ("timeout_s", ctypes.c_double),
                 ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64)]
 
@@ -131,6 +131,7 @@ class Config:
     gc_literal: bool = False
     pr_residue_fp64: bool = False  # fp64 residues (see engine.cuh PrAppT)
     adaptive_fetch: bool = True    # pop min(FETCH, ceil(queued/workers))
+    device_loop: bool = False      # discrete rounds driven on the device (CUDA-graph WHILE node)
     queue_capacity: int = 0
     timeout_s: float = 60.0
     stream: int | None = None      # raw cudaStream_t; None = torch current stream
@@ -150,6 +151,7 @@ class Config:
         c.gc_literal = int(self.gc_literal)
         c.pr_residue_fp64 = int(self.pr_residue_fp64)
         c.adaptive_fetch = int(self.adaptive_fetch)
+        c.device_loop = int(self.device_loop)
         c.queue_capacity = self.queue_capacity
         c.timeout_s = self.timeout_s
         s = self.stream

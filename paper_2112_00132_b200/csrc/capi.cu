@@ -80,6 +80,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->gc_literal = 0;
   c->pr_residue_fp64 = 0;
   c->adaptive_fetch = 1;
+  c->device_loop = 0;
   c->queue_capacity = 0;
   c->timeout_s = 0.0;
   c->stream = nullptr;
@@ -256,6 +257,7 @@ static void graph_free(atos_graph g) {
   cudaFree(w.front[1]);
   cudaFree(w.fcount);
   cudaFree(w.chunks);
+  cudaFree(w.devround);
   if (w.h_ctl) cudaFreeHost(w.h_ctl);
   for (auto& e : w.ev)
     if (e) cudaEventDestroy(e);
@@ -484,9 +486,100 @@ static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_
   return ATOS_OK;
 }
 
+// Discrete strategy with the round loop on the device: a CUDA graph whose
+// WHILE node repeats {one round over [h, t) with a fixed grid, round-end
+// kernel that advances [h, t) and sets the condition}.
+template <class P, class App, int W>
+static atos_status run_discrete_graph_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0) {
+  auto kern = k_discrete_dev<P, App, W>;
+  const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads);
+  const size_t smem = worker_smem_bytes<P>(W, F, T);
+  if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
+  CKS(set_smem(kern, smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
+  const unsigned blocks = (unsigned)std::max(1, per_sm) * (unsigned)c.g->sms;
+  Workspace& w = c.g->ws;
+  if (!w.devround) CK(cudaMalloc(&w.devround, sizeof(DevRound)));
+  DevRound r0{0, t0, 0, 0};
+  CK(cudaMemcpyAsync(w.devround, &r0, sizeof r0, cudaMemcpyHostToDevice, c.s));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  atos_status st = ATOS_OK;
+  do {
+    if (cudaGraphCreate(&graph, 0) != cudaSuccess) { st = atos_set_error(ATOS_ERR_CUDA, "cudaGraphCreate"); break; }
+    cudaGraphConditionalHandle hnd;
+    if (cudaGraphConditionalHandleCreate(&hnd, graph, t0 > 0 ? 1u : 0u, cudaGraphCondAssignDefault) != cudaSuccess) {
+      st = atos_set_error(ATOS_ERR_CUDA, "cudaGraphConditionalHandleCreate");
+      break;
+    }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hnd;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    if (cudaGraphAddNode(&cn, graph, nullptr, 0, &cp) != cudaSuccess) {
+      st = atos_set_error(ATOS_ERR_CUDA, "cudaGraphAddNode(conditional): %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    GraphView gv = c.gv;
+    int Fv = F;
+    const DevRound* rp = w.devround;
+    void* a1[] = {(void*)&app, (void*)&gv, (void*)&q, (void*)&Fv, (void*)&rp};
+    cudaKernelNodeParams k1 = {};
+    k1.func = (void*)kern;
+    k1.gridDim = dim3(blocks);
+    k1.blockDim = dim3(T);
+    k1.sharedMemBytes = (unsigned)smem;
+    k1.kernelParams = a1;
+    cudaGraphNode_t n1, n2;
+    DevRound* rw = w.devround;
+    const QueueCtl* ctl = w.ctl;
+    void* a2[] = {(void*)&rw, (void*)&ctl, (void*)&hnd};
+    cudaKernelNodeParams k2 = {};
+    k2.func = (void*)k_round_end;
+    k2.gridDim = dim3(1);
+    k2.blockDim = dim3(1);
+    k2.kernelParams = a2;
+    if (cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1) != cudaSuccess ||
+        cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2) != cudaSuccess) {
+      st = atos_set_error(ATOS_ERR_CUDA, "cudaGraphAddKernelNode: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      st = atos_set_error(ATOS_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    if (cudaGraphLaunch(exec, c.s) != cudaSuccess) {
+      st = atos_set_error(ATOS_ERR_CUDA, "cudaGraphLaunch: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+  } while (0);
+  (void)cudaGetLastError();
+  if (st == ATOS_OK) {
+    DevRound r1{};
+    CK(cudaMemcpyAsync(&r1, w.devround, sizeof r1, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaStreamSynchronize(c.s));
+    c.rounds += (int64_t)r1.rounds;
+    c.launches += 2 * (int64_t)r1.rounds;
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  return st;
+}
+
 template <class P, class App>
 static atos_status run_discrete(LaunchCtx& c, const App& app, const Queue& q, uint64_t t0, uint64_t h0 = 0,
                                 int64_t max_rounds = -1, uint64_t* h_end = nullptr) {
+  if (c.cfg.device_loop && max_rounds < 0 && h0 == 0) {
+    switch (c.cfg.worker) {
+      case ATOS_WORKER_THREAD: return run_discrete_graph_w<P, App, W_THREAD>(c, app, q, t0);
+      case ATOS_WORKER_WARP: return run_discrete_graph_w<P, App, W_WARP>(c, app, q, t0);
+      default: return run_discrete_graph_w<P, App, W_CTA>(c, app, q, t0);
+    }
+  }
   switch (c.cfg.worker) {
     case ATOS_WORKER_THREAD: return run_discrete_w<P, App, W_THREAD>(c, app, q, t0, h0, max_rounds, h_end);
     case ATOS_WORKER_WARP: return run_discrete_w<P, App, W_WARP>(c, app, q, t0, h0, max_rounds, h_end);

@@ -31,6 +31,7 @@ struct Workspace {
   size_t front_n[2] = {0, 0};
   unsigned long long* fcount = nullptr;
   atos::Chunk* chunks = nullptr;  // hub chunk table
+  struct atos::DevRound* devround = nullptr;  // device-driven discrete rounds
   uint64_t chunk_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };

@@ -192,10 +192,10 @@ __global__ void __launch_bounds__((W == W_CTA && P::kWarpSpecialised) ? CTA_MAX_
 // ------------------------------------------------------------ discrete
 // Round over queue positions [h, t); worker k owns [h + k*chunk, ...).
 template <class P, class App, int W>
-__global__ void __launch_bounds__(1024, 1) k_discrete(App app, GraphView g, Queue q0, uint64_t h, uint64_t t, int F) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  Queue q = q0;
+__device__ __forceinline__ void discrete_round(const App& app, const GraphView& g, Queue& q, uint64_t h, uint64_t t,
+                                               int F, unsigned char* smem) {
   q_arm(q);
+  q.head_floor = t;
   LocalStats st;
   RingSink sink{q};
   const uint64_t S = t - h;
@@ -224,6 +224,36 @@ __global__ void __launch_bounds__(1024, 1) k_discrete(App app, GraphView g, Queu
     }
   }
   st.flush(q);
+}
+
+template <class P, class App, int W>
+__global__ void __launch_bounds__(1024, 1) k_discrete(App app, GraphView g, Queue q0, uint64_t h, uint64_t t, int F) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Queue q = q0;
+  discrete_round<P, App, W>(app, g, q, h, t, F, smem);
+}
+
+// Device-driven discrete strategy: the round snapshot [h, t) lives in device
+// memory and a CUDA-graph WHILE node repeats {k_discrete_dev, k_round_end}
+// until a round produces nothing — one launch of the graph instead of one
+// host round trip per round (the launch overhead the paper measures).
+struct DevRound {
+  uint64_t h, t, rounds, pad;
+};
+
+template <class P, class App, int W>
+__global__ void __launch_bounds__(1024, 1) k_discrete_dev(App app, GraphView g, Queue q0, int F, const DevRound* r) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Queue q = q0;
+  discrete_round<P, App, W>(app, g, q, r->h, r->t, F, smem);
+}
+
+__global__ void k_round_end(DevRound* r, const QueueCtl* ctl, cudaGraphConditionalHandle hnd) {
+  r->h = r->t;
+  r->t = *(volatile const uint64_t*)&ctl->tail.v;
+  r->rounds++;
+  const bool more = r->t > r->h && *(volatile const uint64_t*)&ctl->abort.v == 0;
+  cudaGraphSetConditional(hnd, more ? 1u : 0u);
 }
 
 // ------------------------------------------------------------ BSP

@@ -157,6 +157,22 @@ def test_stats_invariants(atos):
         assert st["kernel_launches"] >= 1 and st["ms"] > 0
 
 
+@pytest.mark.parametrize("worker", WORKERS)
+def test_discrete_device_loop(atos, worker):
+    """Discrete strategy with the round loop in a CUDA-graph WHILE node."""
+    for name in ["rmat16", "grid64", "path"]:
+        d, st = atos.bfs(D(atos, name), 0, kernel="discrete", device_loop=True, worker=worker, fetch_size=16)
+        assert np.array_equal(d, oracle.bfs(G(name), 0)), name
+        d2, st2 = atos.bfs(D(atos, name), 0, kernel="discrete", worker=worker, fetch_size=16)
+        assert st["rounds"] == st2["rounds"], name  # same rounds as the host-driven loop
+    x = jacobi("rmat16")
+    r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel="discrete", device_loop=True, worker=worker,
+                          fetch_size=32, pr_residue_fp64=worker == "thread")
+    assert np.max(np.abs(r - x)) / x.max() <= PR_TOL and st["max_residue"] <= 1e-6
+    c, k, st = atos.color(D(atos, "rmat16s", symmetric=True), kernel="discrete", device_loop=True, worker=worker)
+    assert oracle.check_coloring(G("rmat16s"), c)[0] == 0
+
+
 def test_bfs_adaptive_fetch_off(atos):
     d, st = atos.bfs(D(atos, "rmat16"), 0, adaptive_fetch=False)
     assert np.array_equal(d, oracle.bfs(G("rmat16"), 0))
