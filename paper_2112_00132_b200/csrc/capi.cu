@@ -526,7 +526,7 @@ static atos_status run_discrete_graph_w(LaunchCtx& c, const App& app, Queue q, u
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     GraphView gv = c.gv;
     int Fv = F;
-    const DevRound* rp = w.devround;
+    DevRound* rp = w.devround;
     void* a1[] = {(void*)&app, (void*)&gv, (void*)&q, (void*)&Fv, (void*)&rp};
     cudaKernelNodeParams k1 = {};
     k1.func = (void*)kern;

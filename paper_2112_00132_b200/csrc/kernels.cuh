@@ -193,14 +193,24 @@ __global__ void __launch_bounds__((W == W_CTA && P::kWarpSpecialised) ? CTA_MAX_
 // Round over queue positions [h, t); worker k owns [h + k*chunk, ...).
 template <class P, class App, int W>
 __device__ __forceinline__ void discrete_round(const App& app, const GraphView& g, Queue& q, uint64_t h, uint64_t t,
-                                               int F, unsigned char* smem) {
+                                               int F, unsigned char* smem, unsigned long long* claim = nullptr) {
   q_arm(q);
   q.head_floor = t;
   LocalStats st;
   RingSink sink{q};
   const uint64_t S = t - h;
   if (W == W_CTA) {
-    for (uint64_t k = blockIdx.x; k * (uint64_t)F < S; k += gridDim.x) {
+    __shared__ unsigned long long s_k;
+    // static striding for a grid sized to the round (host loop); dynamic
+    // claiming for the fixed persistent-sized grid of the device loop
+    for (uint64_t k = blockIdx.x;; k += gridDim.x) {
+      if (claim) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_k = atomicAdd(claim, 1ull);
+        __syncthreads();
+        k = s_k;
+      }
+      if (k * (uint64_t)F >= S) break;
       const uint64_t first = h + k * (uint64_t)F;
       const uint32_t n = (uint32_t)umin64((uint64_t)F, t - first);
       RingSrc src{q, first};
@@ -212,7 +222,13 @@ __device__ __forceinline__ void discrete_round(const App& app, const GraphView& 
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nw = (uint64_t)gridDim.x * wpb;
     uint32_t* stage = reinterpret_cast<uint32_t*>(smem) + (size_t)(threadIdx.x >> 5) * chunk;
-    for (uint64_t k = blockIdx.x * wpb + (threadIdx.x >> 5); k * chunk < S; k += nw) {
+    for (uint64_t k = blockIdx.x * wpb + (threadIdx.x >> 5);; k += nw) {
+      if (claim) {
+        unsigned long long kk = 0;
+        if (lane_id() == 0) kk = atomicAdd(claim, 1ull);
+        k = __shfl_sync(FULL_MASK, kk, 0);
+      }
+      if (k * chunk >= S) break;
       const uint64_t first = h + k * chunk;
       const uint32_t n = (uint32_t)umin64(chunk, t - first);
       stage_items(q, first, n, stage);
@@ -238,20 +254,22 @@ __global__ void __launch_bounds__(1024, 1) k_discrete(App app, GraphView g, Queu
 // until a round produces nothing — one launch of the graph instead of one
 // host round trip per round (the launch overhead the paper measures).
 struct DevRound {
-  uint64_t h, t, rounds, pad;
+  uint64_t h, t, rounds;
+  unsigned long long next;  // dynamic chunk claims of the current round
 };
 
 template <class P, class App, int W>
-__global__ void __launch_bounds__(1024, 1) k_discrete_dev(App app, GraphView g, Queue q0, int F, const DevRound* r) {
+__global__ void __launch_bounds__(1024, 1) k_discrete_dev(App app, GraphView g, Queue q0, int F, DevRound* r) {
   extern __shared__ __align__(16) unsigned char smem[];
   Queue q = q0;
-  discrete_round<P, App, W>(app, g, q, r->h, r->t, F, smem);
+  discrete_round<P, App, W>(app, g, q, r->h, r->t, F, smem, &r->next);
 }
 
 __global__ void k_round_end(DevRound* r, const QueueCtl* ctl, cudaGraphConditionalHandle hnd) {
   r->h = r->t;
   r->t = *(volatile const uint64_t*)&ctl->tail.v;
   r->rounds++;
+  r->next = 0;
   const bool more = r->t > r->h && *(volatile const uint64_t*)&ctl->abort.v == 0;
   cudaGraphSetConditional(hnd, more ? 1u : 0u);
 }
