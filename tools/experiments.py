@@ -56,15 +56,17 @@ def kernels():
     print("\n### RMAT-24: persistent vs discrete vs BSP (CTA workers)\n")
     print("| app | kernel | ms | launches | rounds | pops | edges | GTEPS |")
     print("|---|---|---|---|---|---|---|---|")
-    for kern in ["persistent", "discrete", "bsp"]:
-        (d, st), ms = timed(lambda: atos.bfs(G, 0, kernel=kern, fetch_size=128, timeout_s=300), 3)
+    for kern, dl in [("persistent", False), ("discrete", False), ("discrete", True), ("bsp", False)]:
+        (d, st), ms = timed(lambda: atos.bfs(G, 0, kernel=kern, device_loop=dl, fetch_size=128, timeout_s=300), 3)
         e = int(deg[d != atos.UNREACHED].sum())
-        print(f"| BFS | {kern} | {ms:.2f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
+        name = kern + (" (device loop)" if dl else "")
+        print(f"| BFS | {name} | {ms:.2f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
               f"{st['edges_processed']} | {e / ms / 1e6:.1f} |", flush=True)
-    for kern in ["persistent", "discrete", "bsp"]:
-        (r, st), ms = timed(lambda: atos.pagerank(G, 0.85, 1e-6, kernel=kern, fetch_size=128, cta_threads=512,
-                                                  timeout_s=300), 1)
-        print(f"| PageRank | {kern} | {ms:.1f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
+    for kern, dl in [("persistent", False), ("discrete", False), ("discrete", True), ("bsp", False)]:
+        (r, st), ms = timed(lambda: atos.pagerank(G, 0.85, 1e-6, kernel=kern, device_loop=dl, fetch_size=128,
+                                                  cta_threads=512, timeout_s=300), 1)
+        name = kern + (" (device loop)" if dl else "")
+        print(f"| PageRank | {name} | {ms:.1f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
               f"{st['edges_processed']} | {st['edges_processed'] / ms / 1e6:.1f} (raw) |", flush=True)
     (r, st), ms = timed(lambda: atos.pagerank(G, 0.85, 1e-6, pr_activation=1, check_size=8, fetch_size=128,
                                               cta_threads=512, timeout_s=300), 1)
@@ -103,11 +105,16 @@ def grid():
                           ("road-like 4899x4899 (40% edges dropped), src centre", gg.grid(4899, 4899, drop_prob=0.4, seed=3),
                            center)]:
         G = atos.Graph.from_csr(g)
-        for w, t, f in [("cta", 256, 128), ("cta", 64, 16), ("warp", 256, 4), ("thread", 256, 256)]:
-            (d, st), ms = timed(lambda: atos.bfs(G, src, worker=w, cta_threads=t, fetch_size=f, timeout_s=300), 2)
+        for w, t, f, k in [("cta", 256, 128, "persistent"), ("cta", 64, 16, "persistent"), ("warp", 256, 4, "persistent"),
+                           ("thread", 256, 256, "persistent"), ("cta", 256, 128, "discrete"),
+                           ("cta", 256, 128, "discrete+device-loop"), ("cta", 256, 128, "bsp")]:
+            kern = k.split("+")[0]
+            (d, st), ms = timed(lambda: atos.bfs(G, src, worker=w, cta_threads=t, fetch_size=f, kernel=kern,
+                                                 device_loop="device-loop" in k, timeout_s=300), 2)
+            label = f"{w} {k}"
             reached = d != atos.UNREACHED
             e = int(d[reached].max())
-            print(f"| {gname} | {w} ({t}) | {f} | {ms:.1f} | {ms * 1e3 / e:.2f} (ecc {e}, reached "
+            print(f"| {gname} | {label} ({t}) | {f} | {ms:.1f} | {ms * 1e3 / e:.2f} (ecc {e}, reached "
                   f"{int(reached.sum())}) | {st['tasks_popped'] / reached.sum():.3f} |", flush=True)
 
 
