@@ -125,22 +125,6 @@ __global__ void k_max_degree(const int64_t* off, int64_t n, unsigned long long* 
   if (lane_id() == 0) atomicMax(out, m);
 }
 
-// In-degree statistics for hot-destination marking (PageRank push combining).
-__global__ void k_indeg(const int32_t* col, int64_t m, uint32_t* indeg) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(indeg + ((uint32_t)col[e] & COL_MASK), 1u);
-}
-__global__ void k_indeg_hist(const uint32_t* indeg, int64_t n, unsigned long long* hist) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-    if (indeg[v]) atomicAdd(hist + (31 - __clz(indeg[v])), 1ull);
-}
-__global__ void k_mark_hot(int32_t* col, int64_t m, const uint32_t* indeg, uint32_t t) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t w = (uint32_t)col[e] & COL_MASK;
-    if (indeg[w] >= t) col[e] = (int32_t)(w | HOT_BIT);
-  }
-}
-
 static int grid_for(int64_t work, int threads, int sms) {
   int64_t b = (work + threads - 1) / threads;
   int64_t cap = (int64_t)sms * 16;
@@ -201,31 +185,6 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     if (hbad)
       return atos_set_error(ATOS_ERR_INVALID_GRAPH, "CSR validation failed (code %u: 1=non-monotone offsets, "
                             "2=column out of range, 4=off[0]!=0 or off[n]!=m)", hbad);
-  }
-  // hot destinations (owned copies only; a borrowed CSR is never modified):
-  // the <= HOT_MAX vertices of largest in-degree (power-of-two threshold >= 64)
-  if (g->owned && m > 0 && n > 0) {
-    constexpr uint64_t HOT_MAX = 1024;
-    uint32_t* indeg = nullptr;
-    unsigned long long* hist = nullptr;
-    CK(cudaMalloc(&indeg, (size_t)col_bound * sizeof(uint32_t)));
-    CK(cudaMalloc(&hist, 32 * sizeof(unsigned long long)));
-    CK(cudaMemset(indeg, 0, (size_t)col_bound * sizeof(uint32_t)));
-    CK(cudaMemset(hist, 0, 32 * sizeof(unsigned long long)));
-    k_indeg<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, indeg);
-    k_indeg_hist<<<grid_for(col_bound, 256, g->sms), 256>>>(indeg, col_bound, hist);
-    unsigned long long h[32];
-    CK(cudaMemcpy(h, hist, sizeof h, cudaMemcpyDeviceToHost));
-    int b = 31;
-    uint64_t above = h[31];
-    while (b > 6 && above + h[b - 1] <= HOT_MAX) above += h[--b];
-    g->hot_threshold = (above > 0 && above <= HOT_MAX) ? (1u << b) : 0u;
-    g->hot_count = g->hot_threshold ? (int64_t)above : 0;
-    if (g->hot_threshold) k_mark_hot<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, indeg, g->hot_threshold);
-    CK(cudaGetLastError());
-    CK(cudaDeviceSynchronize());
-    cudaFree(indeg);
-    cudaFree(hist);
   }
   unsigned long long* md = reinterpret_cast<unsigned long long*>(g->d_scratch) + 2;
   if (n) k_max_degree<<<grid_for(n, 256, g->sms), 256>>>(g->d_off, n, md);

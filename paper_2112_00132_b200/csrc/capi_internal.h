@@ -46,8 +46,6 @@ struct atos_graph_s {
   int32_t* d_col = nullptr;
   void* d_scratch = nullptr;
   bool owned = false;
-  uint32_t hot_threshold = 0;  // in-degree threshold of HOT_BIT-marked columns (0 = none)
-  int64_t hot_count = 0;
   bool symmetric = false;
   int device = 0;
   int sms = 0;

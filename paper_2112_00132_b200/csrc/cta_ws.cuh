@@ -1,44 +1,18 @@
-// cta_ws.cuh — warp-specialised persistent CTA worker for the edge-map apps
-// (BFS, PageRank): SURVEY §8a rows a4 + a5 on sm_100a.
-//
-// Warp 0 is the CTA's queue agent: it pops the next FETCH-sized batch, reads
-// the claimed slots, runs begin()/chunk/split for every item and scans the
-// degrees into one of two shared-memory batch buffers, while warps 1..W-1
-// expand the other buffer with the load-balancing search.  Pop latency (two
-// L2 atomics), slot reads and the per-vertex begin() loads (dist/off/atomics)
-// thereby overlap the previous batch's edge expansion instead of stalling the
-// whole CTA at a barrier (measured: 24.5% of BFS stall samples sat at the
-// post-pop barrier, profiles/r01_bfs_rmat24_v3).
-//
-// Sync: named barriers.  READY[b] (ids 1,2): agent bar.arrive, workers
-// bar.sync.  FREE[b] (ids 3,4): workers bar.arrive, agent bar.sync.  DONE (id
-// 5): workers only, before the batch's `processed` increment.  The agent reads
-// every claimed slot before it pushes anything (split chunks), so it never
-// waits on a wrapped slot it holds itself.
+// cta_ws.cuh — queue-agent helpers of the persistent CTA worker (SURVEY §8a
+// rows a4 + a5): batch preparation (slot reads, begin loads/atomics, hub
+// splitting) phased for memory-level parallelism, the warp scan, and the
+// Check_Size window activation of Alg. 4 (row f1).  The worker itself is in
+// cta_ws2.cuh.
 #pragma once
-#include <type_traits>
-
 #include "engine.cuh"
 
 namespace atos {
 
-__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <class Payload>
 __host__ __device__ constexpr size_t ws_buf_bytes(int F) {
   return (size_t)F * 8 + ((size_t)F + 1) * 8 + (((size_t)F * sizeof(Payload) + 15) & ~(size_t)15);
 }
-constexpr uint32_t COMB_SLOTS = 2048;  // push-combiner table (2x the hot set)
-template <class Payload>
-__host__ __device__ constexpr size_t comb_bytes() {
-  return (size_t)COMB_SLOTS * (4 + sizeof(Payload) + 4) + 16;
-}
-template <class Payload>
-__host__ __device__ constexpr size_t ws_smem_bytes(int F, bool comb) {
-  return 2 * ws_buf_bytes<Payload>(F) + 64 + (comb ? comb_bytes<Payload>() : 0);
-}
-
 // Warp-cooperative exclusive scan of a[0..n) into a[0..n], a[n] = total.
 __device__ __forceinline__ void warp_exclusive_scan(int64_t* a, int n) {
   const int lane = lane_id();
@@ -237,125 +211,6 @@ __device__ __forceinline__ uint32_t window_sweep(const App& app, const Queue& q,
   if (pushed && lane_id() == 0)
     atomicMax(reinterpret_cast<unsigned long long*>(&q.ctl->aux[1].v), (unsigned long long)(s + span));
   return pushed;
-}
-
-template <class App>
-__device__ void cta_ws_persistent(const App& app, const GraphView& g, const Queue& q, int F, unsigned char* smem,
-                                  LocalStats& st) {
-  using Payload = typename App::Payload;
-  const int T = blockDim.x, tid = threadIdx.x, wid = tid >> 5, lane = lane_id();
-  const size_t bb = ws_buf_bytes<Payload>(F);
-  uint32_t* hdr = reinterpret_cast<uint32_t*>(smem + 2 * bb);  // n of buffer 0 / 1
-  auto buf_e0 = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb); };
-  auto buf_pre = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb) + F; };
-  auto buf_pay = [&](int b) { return reinterpret_cast<Payload*>(reinterpret_cast<int64_t*>(smem + b * bb) + 2 * F + 1); };
-  const Queue* cq = q.chunks ? &q : nullptr;
-
-  if (wid == 0) {
-    // ------------------------------------------------ queue agent (warp 0)
-    int b = 0;
-    for (int round = 0;; ++round) {
-      if (round >= 2) bar_sync_n(3 + b, T);  // workers released buffer b
-      uint64_t first = 0;
-      uint32_t n = 0;
-      if constexpr (App::kWindow) {
-        n = window_pop(app, q, (uint32_t)F, first, st.hw);
-      } else {
-        if (lane == 0) n = q_pop_or_quit(q, (uint32_t)F, first, st.hw);
-        n = __shfl_sync(FULL_MASK, n, 0);
-        first = __shfl_sync(FULL_MASK, first, 0);
-      }
-      int64_t* e0 = buf_e0(b);
-      int64_t* pre = buf_pre(b);
-      Payload* pay = buf_pay(b);
-      if (n) {
-        agent_prepare(app, g, q, cq, first, n, e0, pre, pay);
-        warp_exclusive_scan(pre, (int)n);
-      }
-      if (lane == 0) hdr[b] = n;
-      bar_arrive_n(1 + b, T);  // buffer b ready (n == 0: quit)
-      if (n == 0) {
-        if (round >= 1) bar_sync_n(3 + (b ^ 1), T);  // consume the workers' last release
-        break;
-      }
-      b ^= 1;
-    }
-  } else {
-    // ------------------------------------------------ edge workers (warps 1..W-1)
-    RingSink sink{q};
-    const int nw = (T >> 5) - 1;
-    int b = 0;
-    uint32_t pushed = 0;
-    uint64_t edges = 0;
-    // PageRank: shared-memory combiner for hot destinations
-    using Comb = typename std::conditional<App::kCombine, SmemComb<Payload>, NoComb>::type;
-    Comb comb{};
-    if constexpr (App::kCombine) {
-      unsigned char* cb = smem + 2 * bb + 64;
-      comb.key = reinterpret_cast<uint32_t*>(cb);
-      comb.val = reinterpret_cast<Payload*>(cb + COMB_SLOTS * 4);
-      comb.used = reinterpret_cast<uint32_t*>(cb + COMB_SLOTS * (4 + sizeof(Payload)));
-      comb.nused = comb.used + COMB_SLOTS;
-      comb.mask = COMB_SLOTS - 1;
-      for (uint32_t i = tid - 32; i < COMB_SLOTS; i += T - 32) {
-        comb.key[i] = SmemComb<Payload>::EMPTY;
-        comb.val[i] = Payload(0);
-      }
-      if (tid == 32) *comb.nused = 0;
-      bar_sync_n(5, T - 32);
-    }
-    for (;;) {
-      bar_sync_n(1 + b, T);
-      const uint32_t n = hdr[b];
-      if (n == 0) break;
-      const int64_t* pre = buf_pre(b);
-      const int64_t total = pre[n];
-      pushed += lbs_expand(app, g, sink, pre, buf_e0(b), buf_pay(b), (int)n, total, wid - 1, nw, comb);
-      edges += total;
-      bar_sync_n(5, T - 32);  // every worker's pushes for this batch are reserved
-      if constexpr (App::kWindow) {
-        // Alg. 4 lines 11-14: each popped vertex checks a Check_Size window;
-        // the batch's n * Check_Size ids are split over the worker warps
-        pushed += window_sweep(app, q, (n * (uint32_t)app.check_size + nw - 1) / nw);
-        bar_sync_n(5, T - 32);
-      }
-      if constexpr (App::kCombine) {
-        // flush: one global atomic per combined destination; push on a crossing
-        const uint32_t nu = *comb.nused;
-        for (uint32_t ib = (uint32_t)(wid - 1) * 32; ib < nu; ib += (uint32_t)nw * 32) {
-          const uint32_t i = ib + lane;
-          bool act[1] = {false};
-          uint32_t item[1] = {0};
-          if (i < nu) {
-            const uint32_t h = comb.used[i];
-            const uint32_t w = comb.key[h];
-            const Payload c = comb.val[h];
-            comb.key[h] = SmemComb<Payload>::EMPTY;
-            comb.val[h] = Payload(0);
-            act[0] = app.decide(c, w, 0, app.issue(c, w, 0));
-            item[0] = app.item_of(w);
-          }
-          pushed += sink.template warp_push_multi<1>(act, item);
-        }
-        bar_sync_n(5, T - 32);
-        if (tid == 32) *comb.nused = 0;
-      }
-      if (tid == 32) {
-        st.popped += n;
-        if constexpr (App::kWindow) {  // this batch's residue adds precede the sweep positions after it
-          __threadfence();
-          atomicMax(reinterpret_cast<unsigned long long*>(&q.ctl->aux[2].v),
-                    (unsigned long long)ld_relaxed_u64(&q.ctl->aux[0].v));
-        }
-        q_done(q, n);
-        q_trace(q, n, (uint64_t)total);
-      }
-      bar_arrive_n(3 + b, T);  // release buffer b
-      b ^= 1;
-    }
-    if (lane == 0) st.pushed += pushed;
-    if (tid == 32) st.edges += edges;
-  }
 }
 
 }  // namespace atos

@@ -122,28 +122,18 @@ __device__ __forceinline__ uint64_t pol_evict_last() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// Column words: bit 31 flags a "hot" destination (in-degree above the graph's
-// hot threshold; set once at graph creation on owned copies, see capi.cu
-// mark_hot) — vertex ids are < 2^31 - 1.  PageRank combines pushes to hot
-// destinations in shared memory; every other reader masks the bit off.
-constexpr uint32_t HOT_BIT = 0x80000000u;
-constexpr uint32_t COL_MASK = 0x7FFFFFFFu;
 // streaming read-only loads of immutable CSR arrays (no L1 allocation, L2 evict-first)
 __device__ __forceinline__ int32_t ld_col_raw(const int32_t* p) {
   int32_t v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_first()));
   return v;
 }
-__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p) { return (int32_t)((uint32_t)ld_col_raw(p) & COL_MASK); }
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p) { return ld_col_raw(p); }
 __device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
   int4 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p), "l"(pol_evict_first()));
-  v.x &= COL_MASK;
-  v.y &= COL_MASK;
-  v.z &= COL_MASK;
-  v.w &= COL_MASK;
   return v;
 }
 // hot per-vertex state: relaxed gpu-scope atomics / loads with L2 evict_last

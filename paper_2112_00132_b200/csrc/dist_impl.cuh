@@ -37,7 +37,6 @@ struct Outbox {
 // sends so a remote vertex is sent once per improvement of its tentative depth.
 struct BfsPartApp {
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   uint32_t* dist;
   uint32_t* done;
@@ -99,7 +98,6 @@ struct BfsPartApp {
 template <class R>
 struct PrPartAppT {
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = true;
   static constexpr bool kWindow = false;
   double* rank;
   R* res;
@@ -153,7 +151,6 @@ struct PrPartAppT {
 template <class R>
 struct PrPartInitAppT {
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   R* res;
   float* racc;

@@ -37,7 +37,6 @@ struct BfsApp {
   // (169 vs 93 ms: kept items wait in the CTA's batch pipeline) and 6.8x
   // overwork on the road-like grid, so it is off for every app.
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   uint32_t* dist;
@@ -127,7 +126,6 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 template <class R>
 struct PrAppT {
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = true;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   double* rank;
@@ -187,7 +185,6 @@ struct PrAppT {
 template <class R>
 struct PrWindowAppT {
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = false;
   static constexpr bool kWindow = true;
   double* rank;
   R* res;
@@ -241,7 +238,6 @@ struct PrWindowAppT {
 template <class R>
 struct PrBspAppT {
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   PrAppT<R> base;
@@ -438,44 +434,7 @@ __device__ __forceinline__ const Queue* chunk_queue(const RingSrc& s) { return s
 // lane locates its edges' items by binary search bounded by the owners of the
 // warp's first and last edge, loads UNROLL columns, issues UNROLL probes, then
 // UNROLL commits, then ONE aggregated push.  Returns the pushes (per lane 0).
-// No push combining (BFS, and every non-warp-specialised path).
-struct NoComb {
-  static constexpr bool kOn = false;
-  template <class P>
-  __device__ __forceinline__ bool add(uint32_t, P) const { return false; }
-};
 
-// Shared-memory push combiner for PageRank: contributions to HOT_BIT-marked
-// destinations (the graph's highest in-degree vertices) are summed in a
-// direct-mapped table and applied with ONE global atomic per destination per
-// batch (at flush), instead of one per edge.  Same-address atomics serialise
-// in L2: on RMAT the top vertex alone receives ~0.2% of all PR pushes.  An add
-// is a delayed, merged residue update, so threshold-crossing activation (R6)
-// is unchanged: the flush's atomic sees the old residue and pushes on a crossing.
-template <class R>
-struct SmemComb {
-  static constexpr bool kOn = true;
-  static constexpr uint32_t EMPTY = 0xFFFFFFFFu;
-  uint32_t* key;
-  R* val;
-  uint32_t* used;
-  uint32_t* nused;
-  uint32_t mask;  // table size - 1
-  __device__ __forceinline__ bool add(uint32_t w, R c) const {
-    const uint32_t h = (w * 0x9E3779B1u) >> 7 & mask;
-    uint32_t k = key[h];
-    if (k == EMPTY) {
-      k = atomicCAS(key + h, EMPTY, w);
-      if (k == EMPTY) {
-        k = w;
-        used[atomicAdd(nused, 1u)] = h;
-      }
-    }
-    if (k != w) return false;  // collision with another hot vertex: global path
-    atomicAdd(val + h, c);
-    return true;
-  }
-};
 
 // One LBS step: the warp expands flattened edges [eb, eb + 32*UNROLL) of a
 // prepared batch (see lbs_expand).  Returns the pushes (warp-uniform).
@@ -531,10 +490,10 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
   return sink.template warp_push_multi<U>(act, item);
 }
 
-template <class App, class Sink, class Comb = NoComb>
+template <class App, class Sink>
 __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
                                                const int64_t* e0s, const typename App::Payload* pay, int n,
-                                               int64_t total, int wi, int nw, const Comb& comb = Comb{}) {
+                                               int64_t total, int wi, int nw) {
   const int lane = lane_id();
   const int64_t stride = (int64_t)nw * 32 * LBS_UNROLL;
   uint32_t pushed = 0;
@@ -574,13 +533,6 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
       idx[k] = idxn[k];
     }
     if (eb + stride < total) fetch(eb + stride, wn, idxn);
-    if (Comb::kOn) {
-#pragma unroll
-      for (int k = 0; k < LBS_UNROLL; ++k)
-        if (idx[k] >= 0 && (w[k] & HOT_BIT) && comb.add(w[k] & COL_MASK, pay[idx[k]])) idx[k] = -1;
-    }
-#pragma unroll
-    for (int k = 0; k < LBS_UNROLL; ++k) w[k] &= COL_MASK;
     typename App::Probe pr[LBS_UNROLL];
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k)

@@ -373,7 +373,6 @@ __global__ void k_bfs_init(uint32_t* dist, uint32_t* done, uint16_t* near, int64
 template <class R>
 struct PrInitAppT {
   static constexpr bool kKeep = false;
-  static constexpr bool kCombine = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   R* res;
