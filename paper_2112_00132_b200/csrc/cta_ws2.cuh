@@ -114,7 +114,8 @@ __device__ __forceinline__ void vstore(int* p, int v) { *(volatile int*)p = v; }
 // the `keep` flag (global queue short => workers keep their activations).
 __device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& hw, int nw,
                                               const uint32_t* lrings, int* lhead, const int* ltail, int* keep,
-                                              uint32_t* gather, bool& from_local, bool allow_keep) {
+                                              uint32_t* gather, bool& from_local, bool allow_keep,
+                                              long long& last_count) {
   const int lane = lane_id();
   unsigned ns = 0;
   for (;;) {
@@ -147,24 +148,22 @@ __device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uin
       return got;
     }
     from_local = false;
-    // 2. global queue
+    // 2. global queue (abort / watchdog are checked on the idle path only)
     uint32_t n = 0;
     uint64_t qlen = 0;
     bool quit = false;
     if (lane == 0) {
-      if (q_aborted(q) || q_timed_out(q)) {
+      n = q_try_pop(q, want, first, qlen, last_count);
+      last_count = (long long)qlen - (long long)n;
+      if (allow_keep) *(volatile int*)keep = last_count < (long long)q.workers * 2 ? 1 : 0;
+      if (n) {
+        if (qlen > hw) hw = qlen;
+      } else if (q_aborted(q) || q_timed_out(q)) {
         quit = true;
       } else {
-        n = q_try_pop(q, want, first, qlen);
-        const long long cnt = (long long)ld_relaxed_u64(&q.ctl->count.v);
-        *(volatile int*)keep = (allow_keep && cnt < (long long)q.workers * 2) ? 1 : 0;
-        if (n) {
-          if (qlen > hw) hw = qlen;
-        } else {
-          const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
-          const uint64_t t = q_enqueued(q);
-          quit = p == t;
-        }
+        const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
+        const uint64_t t = q_enqueued(q);
+        quit = p == t;
       }
     }
     n = __shfl_sync(FULL_MASK, n, 0);
@@ -201,6 +200,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
 
   if (wid == 0) {
     // ------------------------------------------------ queue agent
+    long long last_count = 0;  // lane 0: queue length seen at the last pop
     for (int i = 0;; ++i) {
       const int b = i % NBUF;
       // wait until the workers have released buffer b
@@ -220,7 +220,8 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       if constexpr (App::kWindow) {
         n = window_pop(app, q, (uint32_t)F, first, st.hw);
       } else {
-        n = agent_pop(q, (uint32_t)F, first, st.hw, nw, lrings, lhead, ltail, keep, gather, from_local, App::kKeep);
+        n = agent_pop(q, (uint32_t)F, first, st.hw, nw, lrings, lhead, ltail, keep, gather, from_local, App::kKeep,
+                      last_count);
       }
       if (n) {
         agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b), from_local ? gather : nullptr);
