@@ -77,6 +77,9 @@ typedef struct {
   void* stream;           /* cudaStream_t to run on; NULL = legacy default stream             */
   void* trace;            /* optional device buffer of atos_trace_rec (timeline);  */
   int64_t trace_capacity; /*   records; one per processed batch; extra records are dropped    */
+  int32_t stage_edges;    /* persistent CTA workers: column-list staging per batch buffer via   */
+                          /*   TMA bulk copies, in edges; -1 = auto, 0 = off       */
+  int32_t _pad0;
 } atos_config;
 
 /* One timeline record per batch processed by a persistent/discrete worker:

@@ -54,7 +54,8 @@ class CConfig(ctypes.Structure):
                 ("gc_literal", ctypes.c_int32), ("pr_residue_fp64", ctypes.c_int32),
                 ("adaptive_fetch", ctypes.c_int32), ("device_loop", ctypes.c_int32),
                 ("queue_capacity", ctypes.c_int64), ("timeout_s", ctypes.c_double),
-                ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64)]
+                ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64),
+                ("stage_edges", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
 
 
 class CStats(ctypes.Structure):
@@ -136,6 +137,7 @@ class Config:
     timeout_s: float = 60.0
     stream: int | None = None      # raw cudaStream_t; None = torch current stream
     trace: object = None           # Trace() buffer for the timeline, or None
+    stage_edges: int = -1          # TMA column staging per batch buffer (edges); -1 auto, 0 off
 
     def to_c(self) -> CConfig:
         c = CConfig()
@@ -154,6 +156,7 @@ class Config:
         c.device_loop = int(self.device_loop)
         c.queue_capacity = self.queue_capacity
         c.timeout_s = self.timeout_s
+        c.stage_edges = self.stage_edges
         s = self.stream
         if s is None:
             import torch

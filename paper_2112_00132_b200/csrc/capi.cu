@@ -84,6 +84,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->queue_capacity = 0;
   c->timeout_s = 0.0;
   c->stream = nullptr;
+  c->stage_edges = -1;
 }
 
 static atos_status check_config(const atos_config* c) {
@@ -102,6 +103,8 @@ static atos_status check_config(const atos_config* c) {
   if (c->pr_activation != 0 && c->pr_activation != 1)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "pr_activation must be 0 or 1");
   if (c->trace && c->trace_capacity < 0) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "trace_capacity < 0");
+  if (c->stage_edges < -1 || c->stage_edges > (1 << 20))
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "stage_edges %d not in [-1, 2^20]", c->stage_edges);
   if (c->pr_activation == 1 && c->check_size < 1)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "check_size < 1");
   return ATOS_OK;
@@ -153,10 +156,13 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
   if (borrow) {
     g->d_off = const_cast<int64_t*>(off);
     g->d_col = const_cast<int32_t*>(col);
+    g->col_cap = m;
     g->owned = false;
   } else {
     CK(cudaMalloc(&g->d_off, (size_t)(n + 1) * sizeof(int64_t)));
-    CK(cudaMalloc(&g->d_col, (size_t)std::max<int64_t>(m, 4) * sizeof(int32_t)));
+    g->col_cap = ((m + 3) & ~(int64_t)3) + 4;  // padded: 16-B bulk copies may overrun a list's end
+    CK(cudaMalloc(&g->d_col, (size_t)g->col_cap * sizeof(int32_t)));
+    CK(cudaMemset(g->d_col, 0, (size_t)g->col_cap * sizeof(int32_t)));
     g->owned = true;
     CK(cudaMemcpy(g->d_off, off, (size_t)(n + 1) * sizeof(int64_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
     if (m) CK(cudaMemcpy(g->d_col, col, (size_t)m * sizeof(int32_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
@@ -362,6 +368,22 @@ static int clamp_threads(int W, int F, int T, bool ws = false) {
   return std::min(T, max_warps * 32);
 }
 
+// Staged column elements per batch buffer: `req` (>0: as requested, -1: auto)
+// rounded to a multiple of 4, bounded so per_sm CTAs still fit in the SM's
+// shared memory with `l1_keep` bytes left to L1 (the BFS probes and PR
+// residue atomics go through it).  ATOS_STAGE_EDGES overrides (experiments).
+static int stage_capacity(int req, int per_sm, size_t base_smem) {
+  if (const char* e = getenv("ATOS_STAGE_EDGES")) req = atoi(e);
+  if (req == 0) return 0;
+  const size_t sm_total = 228 * 1024, per_block_reserved = 1024, l1_keep = 64 * 1024;
+  const size_t budget = (sm_total - l1_keep) / (size_t)per_sm;
+  if (budget <= base_smem + per_block_reserved) return 0;
+  size_t fit = (budget - base_smem - per_block_reserved) / (NBUF * 4);
+  size_t want = req > 0 ? (size_t)req : 4096;
+  size_t S = std::min(fit, want) & ~(size_t)3;
+  return S >= 256 ? (int)S : 0;
+}
+
 template <class P, class App, int W>
 static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q) {
   auto kern = k_persistent<P, App, W>;
@@ -376,13 +398,24 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
     qq.chunks = w.chunks;
     qq.chunk_mask = w.chunk_cap - 1;
   }
-  const size_t smem = worker_smem_bytes<P>(W, F, T, true);
+  size_t smem = worker_smem_bytes<P>(W, F, T, true);
   if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
   if (W == W_CTA && P::kWarpSpecialised && T < 64)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "persistent CTA workers need cta_threads >= 64 (1 queue warp + workers)");
   CKS(set_smem(kern, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
+  if (W == W_CTA && P::kWarpSpecialised && per_sm >= 1) {
+    // Column staging (TMA bulk copies into each batch buffer): the capacity
+    // that keeps the register-limited CTAs per SM resident, minus an L1 share.
+    const int S = stage_capacity(c.cfg.stage_edges, per_sm, smem);
+    if (S > 0) {
+      qq.stage_cap = (uint32_t)S;
+      smem = worker_smem_bytes<P>(W, F, T, true, S);
+      CKS(set_smem(kern, smem));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
+    }
+  }
   if (per_sm < 1) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "kernel cannot be resident with %d threads", T);
   int blocks = per_sm * c.g->sms;
   if (c.cfg.num_blocks > 0) blocks = std::min(blocks, c.cfg.num_blocks);  // persistent: <= resident maximum
@@ -614,6 +647,18 @@ static atos_status finish_stats(LaunchCtx& c, atos_stats* st, bool bsp) {
     st->rounds = c.rounds;
     st->queue_high_water = bsp ? (int64_t)w.h_ctl->high_water.v : (int64_t)w.h_ctl->high_water.v;
   }
+#ifdef ATOS_WAIT_PROF
+  {
+    const QueueCtl* h = w.h_ctl;
+    fprintf(stderr, "ATOS_PROF Mcycles agent: wait_free %.1f pop %.1f prep %.1f | workers: wait_ready %.1f steps %.1f exit %.1f\n",
+            h->prof[0].v * 1e-6, h->prof[1].v * 1e-6, h->prof[2].v * 1e-6, h->prof[3].v * 1e-6, h->prof[4].v * 1e-6,
+            h->prof[5].v * 1e-6);
+    if (h->prof[9].v)
+      fprintf(stderr, "ATOS_PROF step cycles: %.0f steps, col %.0f, probe+atomic+decide %.0f, push %.0f (mean per step)\n",
+              (double)h->prof[9].v, (double)h->prof[6].v / h->prof[9].v, (double)h->prof[7].v / h->prof[9].v,
+              (double)h->prof[8].v / h->prof[9].v);
+  }
+#endif
   return ATOS_OK;
 }
 
@@ -630,7 +675,7 @@ static atos_status begin_call(atos_graph g, const atos_config* cfg_in, LaunchCtx
   }
   c.g = g;
   c.s = reinterpret_cast<cudaStream_t>(c.cfg.stream);
-  c.gv = GraphView{g->d_off, g->d_col, g->n};
+  c.gv = GraphView{g->d_off, g->d_col, g->n, g->col_cap};
   c.t0 = std::chrono::steady_clock::now();
   int dev = 0;
   CK(cudaGetDevice(&dev));

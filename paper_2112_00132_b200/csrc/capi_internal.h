@@ -44,6 +44,7 @@ struct atos_graph_s {
   int64_t max_degree = 0;
   int64_t* d_off = nullptr;
   int32_t* d_col = nullptr;
+  int64_t col_cap = 0;  // readable elements of d_col
   void* d_scratch = nullptr;
   bool owned = false;
   bool symmetric = false;

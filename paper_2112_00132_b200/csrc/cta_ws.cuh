@@ -46,7 +46,7 @@ constexpr int AGENT_G = 4;
 template <class App>
 __device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g, const Queue& q, const Queue* cq,
                                               uint64_t first, uint32_t n, int64_t* e0s, int64_t* pre,
-                                              typename App::Payload* pay, const uint32_t* local_items = nullptr) {
+                                              typename App::Payload* pay) {
   using Payload = typename App::Payload;
   using Pre = typename App::Pre;
   const uint32_t lane = lane_id();
@@ -57,15 +57,13 @@ __device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g
 #pragma unroll
     for (int k = 0; k < AGENT_G; ++k) {
       const uint32_t i = base + lane + 32 * k;
-      raw[k] = (i < n && !local_items) ? ld_relaxed_u64(q.ring + ((first + i) & q.mask)) : 0;
+      raw[k] = i < n ? ld_relaxed_u64(q.ring + ((first + i) & q.mask)) : 0;
     }
 #pragma unroll
     for (int k = 0; k < AGENT_G; ++k) {
       const uint32_t i = base + lane + 32 * k;
       it[k] = 0xFFFFFFFFu;
-      if (i < n && local_items) {
-        it[k] = local_items[i];  // a CTA-local continuation item (already counted in tail)
-      } else if (i < n) {
+      if (i < n) {
         const uint64_t p = first + i;
         const uint32_t want = 2u * (uint32_t)(p >> q.log2cap) + 1u;
         if ((uint32_t)(raw[k] >> 32) == want) {

@@ -3,29 +3,28 @@
 //
 // Warp 0 (the queue agent) pops FETCH-sized batches, reads their slots, runs
 // begin()/chunk/split and scans degrees into a ring of NBUF shared-memory batch
-// buffers, up to NBUF-1 batches ahead.  Worker warps 1..W-1 consume the ring
-// in order, claiming 32*UNROLL-edge steps of the current batch with a
-// shared-memory atomic; a warp that finds the batch exhausted moves on to the
-// next batch at once — no CTA barrier per batch.  The last warp to leave a
-// batch increments `processed` (a7; every warp's pushes for the batch are
-// reserved before it leaves) and frees the buffer.  (The double-buffered
-// version with bar.sync hand-offs spent 20-27% of its stall samples in
-// barriers, profiles/r01_*_ncu.md.)
+// buffers, up to NBUF-1 batches ahead.  It also stages the batch's column lists
+// into the buffer with TMA 1-D bulk copies (cp.async.bulk, completion on a
+// per-buffer mbarrier), so worker warps read neighbour ids from shared memory
+// instead of waiting on DRAM ("lists ... staged into smem
+// by cp.async.bulk (TMA 1-D bulk copy), double-buffered" — here NBUF-buffered).
+// Worker warps 1..W-1 consume the ring in order, claiming 32*UNROLL-edge steps
+// of the current batch with a shared-memory atomic; a warp that finds the
+// batch exhausted moves on to the next batch at once — no CTA barrier per
+// batch.  The last warp to leave a batch increments `processed` (a7; every
+// warp's pushes for the batch are reserved before it leaves) and frees the
+// buffer.  (The double-buffered version with bar.sync hand-offs spent 20-27%
+// of its stall samples in barriers, profiles/r01_*_ncu.md.)
 #pragma once
 #include "cta_ws.cuh"
 
 namespace atos {
 
-constexpr int NBUF = 4;
-// CTA-local continuation (small-frontier regime): while the global queue is
-// short, a worker warp keeps the vertices it activates in its own SPSC ring in
-// shared memory and the CTA's agent takes them next, skipping the global
-// push -> poll -> pop round trip on the critical path of high-diameter
-// graphs (9.5 us per hop on the 4899^2 grid without it).  Kept items are
-// counted in ctl->kept (they take no ring position), and quiescence (a7) is
-// processed == tail + kept.
-constexpr int LCAP = 128;  // per worker warp
-constexpr int STEP_CAP = 2048;  // per-buffer step-owner table (steps beyond it search)
+#ifndef ATOS_NBUF
+#define ATOS_NBUF 4
+#endif
+constexpr int NBUF = ATOS_NBUF;
+constexpr int STEP_CAP = 512;  // per-buffer step-owner table (u16; steps beyond it binary-search)
 // Register budget vs occupancy of the persistent CTA kernel (build-time knobs).
 // Measured on RMAT-24 (PR kernel ms / BFS ms): 1024x1 bound (64 regs, some
 // spills) + unroll 8: 209 / 4.1 — best; 512x1 (128 regs) + unroll 16:
@@ -44,7 +43,27 @@ constexpr int CTA_MAX_THREADS = ATOS_CTA_MAX_THREADS;
 constexpr int CTA_MIN_BLOCKS = ATOS_CTA_MIN_BLOCKS;
 constexpr int WS_UNROLL = ATOS_WS_UNROLL;
 constexpr int64_t STEP_EDGES = 32 * WS_UNROLL;
+// Column staging: item i of a batch is staged at element offset
+// roundup4(pre[i] + STAGE_PAD * i) of the buffer's stage area, covering its
+// 16-B aligned superset [e0 & ~3, roundup4(e1)) (at most 6 extra elements), so
+// slots never overlap and need no second scan; an item is staged iff its slot
+// ends within the stage capacity (so the staged items are a prefix).
+constexpr int STAGE_PAD = 10;
 enum : int { BUF_FREE = 0, BUF_READY = 1, BUF_QUIT = 2 };
+
+// ATOS_WAIT_PROF builds (tuning experiments only) accumulate clock64 cycles per
+// phase into ctl->prof: 0 agent waits for a free buffer, 1 agent pop, 2 agent
+// prepare + scan + staging issue, 3 workers wait for a ready buffer (and its
+// staged columns), 4 workers in steps, 5 worker batch exits.
+#ifdef ATOS_WAIT_PROF
+#define WPROF_DECL long long wp_t = clock64(); unsigned long long wp_acc[6] = {0, 0, 0, 0, 0, 0};
+#define WPROF_MARK(i) do { const long long wp_n = clock64(); wp_acc[i] += (unsigned long long)(wp_n - wp_t); wp_t = wp_n; } while (0)
+#define WPROF_FLUSH(q) do { if (lane_id() == 0) for (int wp_i = 0; wp_i < 6; ++wp_i) if (wp_acc[wp_i]) atomicAdd(reinterpret_cast<unsigned long long*>(&(q).ctl->prof[wp_i].v), wp_acc[wp_i]); } while (0)
+#else
+#define WPROF_DECL
+#define WPROF_MARK(i) do {} while (0)
+#define WPROF_FLUSH(q) do {} while (0)
+#endif
 
 struct BufHdr {
   int state;     // BUF_*
@@ -52,110 +71,47 @@ struct BufHdr {
   int n;         // items
   int next;      // next step index to claim
   int left;      // warps that have left this batch
+  int pad;
   long long total;
 };
 
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+// Per-buffer layout: e0 (F x i64) | pre ((F+1) x i64) | payload (F) |
+// own (STEP_CAP x u16) | sofs (F x i32) | stage (S x i32, 16-B aligned).
 template <class Payload>
-__host__ __device__ constexpr size_t ws2_buf_bytes(int F) {
-  return ws_buf_bytes<Payload>(F) + (size_t)STEP_CAP * 4;
+__host__ __device__ constexpr size_t ws2_sofs_offset(int F) {
+  return align16(ws_buf_bytes<Payload>(F) + (size_t)STEP_CAP * 2);
 }
 template <class Payload>
-__host__ __device__ constexpr size_t ws2_smem_bytes(int F) {
-  // + local rings (31 worker warps max) + their head/tail + the agent's gather scratch
-  return (size_t)NBUF * ws2_buf_bytes<Payload>(F) + NBUF * sizeof(BufHdr) + 64 + 31 * LCAP * 4 + 64 * 4 +
-         ((size_t)F * 4 + 16);
+__host__ __device__ constexpr size_t ws2_stage_offset(int F) {
+  return ws2_sofs_offset<Payload>(F) + align16((size_t)F * 4);
 }
-
-// Worker-side sink: keep activated items in the warp's local ring when the
-// agent says the global queue is short and the ring has room; else push globally.
-struct KeepSink {
-  Queue q;
-  uint32_t* ring;          // this warp's LCAP slots
-  int* tail;               // producer index (this warp)
-  const int* head;         // consumer index (agent)
-  const int* keep;         // agent's "queue is short" flag
-  template <int U>
-  __device__ __forceinline__ uint32_t warp_push_multi(const bool (&pred)[U], const uint32_t (&item)[U]) const {
-    unsigned m[U];
-    uint32_t total = 0;
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      m[k] = __ballot_sync(FULL_MASK, pred[k]);
-      total += __popc(m[k]);
-    }
-    if (total == 0) return 0;
-    const int t = *(volatile const int*)tail;
-    const bool local = *(volatile const int*)keep && (int)total <= LCAP - (t - *(volatile const int*)head);
-    if (!local) return q_warp_push_multi<U>(q, pred, item);
-    if (lane_id() == 0)  // count the kept items as enqueued (termination); wait for it to be performed
-      (void)atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->kept.v), (unsigned long long)total);
-    const unsigned lt = lanemask_lt();
-    int base = t;
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      if (pred[k]) ring[(base + __popc(m[k] & lt)) % LCAP] = item[k];
-      base += __popc(m[k]);
-    }
-    __syncwarp();
-    if (lane_id() == 0) {
-      __threadfence_block();
-      *(volatile int*)tail = t + (int)total;
-    }
-    __syncwarp();
-    return total;
-  }
-};
+template <class Payload>
+__host__ __device__ constexpr size_t ws2_buf_bytes(int F, int S) {
+  return ws2_stage_offset<Payload>(F) + (size_t)S * 4;
+}
+template <class Payload>
+__host__ __device__ constexpr size_t ws2_smem_bytes(int F, int S) {
+  // buffers + headers + one mbarrier per buffer
+  return (size_t)NBUF * ws2_buf_bytes<Payload>(F, S) + NBUF * sizeof(BufHdr) + NBUF * 8;
+}
 
 __device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
 __device__ __forceinline__ void vstore(int* p, int v) { *(volatile int*)p = v; }
 
-// Agent pop: CTA-local continuation items first, then the global queue; the
-// idle path polls both and runs the termination check (a7).  Also maintains
-// the `keep` flag (global queue short => workers keep their activations).
-__device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& hw, int nw,
-                                              const uint32_t* lrings, int* lhead, const int* ltail, int* keep,
-                                              uint32_t* gather, bool& from_local, bool allow_keep,
+// Agent pop from the global queue; the idle path runs the termination check (a7).
+__device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& hw,
                                               long long& last_count) {
   const int lane = lane_id();
   unsigned ns = 0;
   for (;;) {
-    // 1. local rings (lane w drains worker warp w's ring)
-    uint32_t got = 0;
-    if (*(volatile int*)keep || true) {
-      int avail = 0, h = 0;
-      if (lane < nw) {
-        h = lhead[lane];
-        avail = *(volatile const int*)(ltail + lane) - h;
-      }
-      // exclusive scan of avail over lanes, capped at want
-      int x = avail;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(FULL_MASK, x, d);
-        if (lane >= d) x += y;
-      }
-      const int before = x - avail;
-      const int take = max(0, min(avail, (int)want - before));
-      __threadfence_block();
-      for (int i = 0; i < take; ++i) gather[before + i] = lrings[lane * LCAP + (h + i) % LCAP];
-      got = (uint32_t)min(__shfl_sync(FULL_MASK, x, 31), (int)want);
-      __syncwarp();
-      if (take) *(volatile int*)(lhead + lane) = h + take;
-      __syncwarp();
-    }
-    if (got) {
-      from_local = true;
-      return got;
-    }
-    from_local = false;
-    // 2. global queue (abort / watchdog are checked on the idle path only)
+    // abort / watchdog are checked on the idle path only
     uint32_t n = 0;
     uint64_t qlen = 0;
     bool quit = false;
     if (lane == 0) {
       n = q_try_pop(q, want, first, qlen, last_count);
       last_count = (long long)qlen - (long long)n;
-      if (allow_keep) *(volatile int*)keep = last_count < (long long)q.workers * 2 ? 1 : 0;
       if (n) {
         if (qlen > hw) hw = qlen;
       } else if (q_aborted(q) || q_timed_out(q)) {
@@ -175,32 +131,69 @@ __device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uin
   }
 }
 
+// Agent: stage the column lists of the batch's leading items into `stage`
+// (capacity S elements) with one TMA bulk copy per item, all completing on
+// `bar`; sofs[i] = stage offset of item i's first edge, or -1 (the workers
+// read it from global memory).  Exactly one arrival per batch, so the
+// barrier's k-th phase completes with the k-th use of the buffer.
+__device__ __forceinline__ void agent_stage(const GraphView& g, uint32_t n, const int64_t* e0s, const int64_t* pre,
+                                            int* sofs, int32_t* stage, uint32_t S, uint64_t* bar) {
+  const uint32_t lane = lane_id();
+  uint32_t bytes = 0;
+  for (uint32_t it = lane; it < n; it += 32) {
+    const int64_t deg = pre[it + 1] - pre[it];
+    const int64_t a = e0s[it];
+    const int64_t as = a & ~(int64_t)3, ae = (a + deg + 3) & ~(int64_t)3;
+    const bool st = deg > 0 && pre[it + 1] + (int64_t)STAGE_PAD * (it + 1) <= (int64_t)S && ae <= g.col_cap;
+    const int64_t slot = (pre[it] + (int64_t)STAGE_PAD * it + 3) & ~(int64_t)3;
+    sofs[it] = st ? (int)(slot + (a - as)) : -1;
+    if (st) bytes += (uint32_t)(ae - as) * 4u;
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL_MASK, bytes, d);
+  if (lane == 0) {
+    fence_proxy_async_smem();  // order the workers' reads of the buffer's last batch before the async writes
+    mbar_arrive_expect_tx(bar, bytes);
+  }
+  __syncwarp();
+  if (bytes == 0) return;
+  for (uint32_t it = lane; it < n; it += 32) {
+    const int o = sofs[it];
+    if (o < 0) continue;
+    const int64_t a = e0s[it], deg = pre[it + 1] - pre[it];
+    const int64_t as = a & ~(int64_t)3, ae = (a + deg + 3) & ~(int64_t)3;
+    tma_load_1d(stage + (o - (int)(a - as)), g.col + as, (uint32_t)(ae - as) * 4u, bar);
+  }
+}
+
 template <class App>
 __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Queue& q, int F, unsigned char* smem,
                                    LocalStats& st) {
   using Payload = typename App::Payload;
   const int T = blockDim.x, tid = threadIdx.x, wid = tid >> 5, lane = lane_id();
-  const size_t bb = ws2_buf_bytes<Payload>(F);
+  const uint32_t S = q.stage_cap;
+  const size_t bb = ws2_buf_bytes<Payload>(F, (int)S);
   BufHdr* hdr = reinterpret_cast<BufHdr*>(smem + NBUF * bb);
-  auto buf_own = [&](int b) { return reinterpret_cast<int*>(smem + b * bb + ws_buf_bytes<Payload>(F)); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(hdr + NBUF);
+  auto buf_own = [&](int b) { return reinterpret_cast<uint16_t*>(smem + b * bb + ws_buf_bytes<Payload>(F)); };
   auto buf_e0 = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb); };
   auto buf_pre = [&](int b) { return reinterpret_cast<int64_t*>(smem + b * bb) + F; };
   auto buf_pay = [&](int b) { return reinterpret_cast<Payload*>(reinterpret_cast<int64_t*>(smem + b * bb) + 2 * F + 1); };
+  auto buf_sofs = [&](int b) { return reinterpret_cast<int*>(smem + b * bb + ws2_sofs_offset<Payload>(F)); };
+  auto buf_stage = [&](int b) { return reinterpret_cast<int32_t*>(smem + b * bb + ws2_stage_offset<Payload>(F)); };
   const Queue* cq = q.chunks ? &q : nullptr;
   const int nw = (T >> 5) - 1;
-  uint32_t* lrings = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(hdr + NBUF) + 64);
-  int* lhead = reinterpret_cast<int*>(lrings + 31 * LCAP);  // [32]
-  int* ltail = lhead + 32;                                  // [32]
-  int* keep = ltail + 31;                                   // shares the last tail slot (31 warps max)
-  uint32_t* gather = reinterpret_cast<uint32_t*>(ltail + 32);
-  if (tid < 64) lhead[tid] = 0;
-  if (tid == 0) *keep = 0;
-  if (tid < NBUF) hdr[tid] = BufHdr{BUF_FREE, -1, 0, 0, 0, 0};
+  if (tid < NBUF) {
+    hdr[tid] = BufHdr{BUF_FREE, -1, 0, 0, 0, 0, 0};
+    if (S) mbar_init(&bars[tid], 1);
+  }
+  if (S && tid == 0) fence_mbar_init();
   __syncthreads();
 
   if (wid == 0) {
     // ------------------------------------------------ queue agent
     long long last_count = 0;  // lane 0: queue length seen at the last pop
+    WPROF_DECL
     for (int i = 0;; ++i) {
       const int b = i % NBUF;
       // wait until the workers have released buffer b
@@ -214,25 +207,26 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
         __syncwarp();
         break;
       }
+      WPROF_MARK(0);
       uint64_t first = 0;
       uint32_t n = 0;
-      bool from_local = false;
       if constexpr (App::kWindow) {
         n = window_pop(app, q, (uint32_t)F, first, st.hw);
       } else {
-        n = agent_pop(q, (uint32_t)F, first, st.hw, nw, lrings, lhead, ltail, keep, gather, from_local, App::kKeep,
-                      last_count);
+        n = agent_pop(q, (uint32_t)F, first, st.hw, last_count);
       }
+      WPROF_MARK(1);
       if (n) {
-        agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b), from_local ? gather : nullptr);
+        agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b));
         int64_t* pre = buf_pre(b);
         warp_exclusive_scan(pre, (int)n);
+        if (S) agent_stage(g, n, buf_e0(b), pre, buf_sofs(b), buf_stage(b), S, &bars[b]);
         // step-owner table: own[c] = item holding flattened edge c*STEP_EDGES
-        int* own = buf_own(b);
+        uint16_t* own = buf_own(b);
         for (uint32_t it = lane; it < n; it += 32) {
           const int64_t c0 = (pre[it] + STEP_EDGES - 1) / STEP_EDGES;
           const int64_t c1 = min((pre[it + 1] + STEP_EDGES - 1) / STEP_EDGES, (int64_t)STEP_CAP);
-          for (int64_t c = c0; c < c1; ++c) own[c] = (int)it;
+          for (int64_t c = c0; c < c1; ++c) own[c] = (uint16_t)it;
         }
         __syncwarp();
       }
@@ -246,14 +240,16 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
         vstore(&hdr[b].state, n ? BUF_READY : BUF_QUIT);
       }
       __syncwarp();
+      WPROF_MARK(2);
       if (n == 0) break;
     }
+    WPROF_FLUSH(q);
   } else {
     // ------------------------------------------------ edge workers
-    const int wi = wid - 1;
-    KeepSink sink{q, lrings + wi * LCAP, ltail + wi, lhead + wi, keep};
+    RingSink sink{q};
     uint32_t pushed = 0;
     uint64_t edges = 0;
+    WPROF_DECL
     for (int i = 0;; ++i) {
       const int b = i % NBUF, pass = i / NBUF;
       int s = BUF_FREE;
@@ -265,12 +261,20 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       }
       if (s == BUF_QUIT) break;
       __threadfence_block();
+      // this batch's staged columns complete the buffer's pass-th mbarrier phase
+      if (S) {
+        for (unsigned ns = 8; !mbar_try_wait(&bars[b], (uint32_t)pass & 1u); ns = ns < 128 ? ns * 2 : ns)
+          __nanosleep(ns);
+      }
+      WPROF_MARK(3);
       const int n = hdr[b].n;
       const int64_t total = hdr[b].total;
       const int64_t* pre = buf_pre(b);
       const int64_t* e0 = buf_e0(b);
       const Payload* pay = buf_pay(b);
-      const int* own = buf_own(b);
+      const uint16_t* own = buf_own(b);
+      const int* sofs = S ? buf_sofs(b) : nullptr;
+      const int32_t* stage = buf_stage(b);
       const int64_t steps = (total + STEP_EDGES - 1) / STEP_EDGES;
       for (;;) {
         int c = 0;
@@ -282,8 +286,8 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
           hlo = own[c];
           hhi = (c + 1 < steps && c + 1 < STEP_CAP) ? own[c + 1] : n - 1;
         }
-        const uint32_t p = lbs_step<App, KeepSink, WS_UNROLL>(app, g, sink, pre, e0, pay, n, total,
-                                                               (int64_t)c * STEP_EDGES, hlo, hhi);
+        const uint32_t p = lbs_step<App, RingSink, WS_UNROLL>(app, g, sink, pre, e0, pay, n, total,
+                                                               (int64_t)c * STEP_EDGES, hlo, hhi, sofs, stage);
         if (lane == 0) pushed += p;
         if (lane == 0) edges += (uint64_t)min(STEP_EDGES, total - (int64_t)c * STEP_EDGES);
       }
@@ -292,6 +296,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
         pushed += window_sweep(app, q, ((uint32_t)n * (uint32_t)app.check_size + nw - 1) / nw);
       }
       __syncwarp();
+      WPROF_MARK(4);
       int last = 0;
       if (lane == 0) {
         __threadfence_block();
@@ -309,7 +314,9 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
         q_trace(q, (uint32_t)n, (uint64_t)total);
         vstore(&hdr[b].state, BUF_FREE);
       }
+      WPROF_MARK(5);
     }
+    WPROF_FLUSH(q);
     if (lane == 0) {
       st.pushed += pushed;
       st.edges += edges;

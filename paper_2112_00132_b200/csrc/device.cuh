@@ -136,6 +136,37 @@ __device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
                : "l"(p), "l"(pol_evict_first()));
   return v;
 }
+// ---- TMA 1-D bulk copies + mbarriers (column staging for CTA workers, a5)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// one arrival that also adds `bytes` to the phase's expected transaction count
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// global -> shared bulk copy (cp.async.bulk, the TMA unit's 1-D mode): 16-B
+// aligned addresses, size a multiple of 16; completion is signalled on `bar`.
+// Columns stream once per expansion, so the copy reads them L2 evict_first.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol_evict_first())
+      : "memory");
+}
+
 // hot per-vertex state: relaxed gpu-scope atomics / loads with L2 evict_last
 __device__ __forceinline__ uint32_t atom_min_hot(uint32_t* p, uint32_t v) {
   uint32_t o;
@@ -211,9 +242,9 @@ struct QueueCtl {
   Line64 chunk_tail;    // hub chunk table: entries allocated
   Line64 chunk_done;    // hub chunk table: entries consumed
   Line64 trace_count;   // timeline records produced
-  Line64 kept;          // tasks kept in CTA-local continuation rings (no ring position)
   Line64 stats[4];      // popped, pushed, edges, spare
   Line64 aux[4];        // app-specific counters (e.g. PR check cursor, colours)
+  Line64 prof[12];       // clock64 cycle counters of ATOS_WAIT_PROF builds (tuning experiments only)
 };
 
 // Kernel-side view of the queue (passed by value).
@@ -232,6 +263,7 @@ struct Queue {
   uint32_t trace_kind;
   uint32_t workers;  // adaptive fetch: number of concurrent poppers (0 = off)
   uint32_t backoff_ns;  // idle-poll backoff cap
+  uint32_t stage_cap;   // persistent CTA workers: staged column elements per batch buffer (0 = off)
 };
 
 // Timeline record (layout == atos_trace_rec in include/atos.h).
@@ -460,11 +492,11 @@ __device__ __forceinline__ uint32_t q_try_pop(const Queue& q, uint32_t want, uin
   return n;
 }
 
-// Tasks ever enqueued = ring positions handed out (tail) + tasks kept in
-// CTA-local rings.  Read AFTER `processed`: processed <= enqueued always, so
-// equality at the reads implies equality (quiescence) at the processed read.
+// Tasks ever enqueued = ring positions handed out.  Read AFTER `processed`:
+// processed <= enqueued always, so equality at the reads implies equality
+// (quiescence) at the processed read.
 __device__ __forceinline__ uint64_t q_enqueued(const Queue& q) {
-  return ld_relaxed_u64(&q.ctl->tail.v) + ld_relaxed_u64(&q.ctl->kept.v);
+  return ld_relaxed_u64(&q.ctl->tail.v);
 }
 
 // Leader-side pop with the idle path (the paper's f2 hook): backoff,

@@ -36,7 +36,6 @@ struct Outbox {
 // BFS on a partition: dist/done are local; sent_min (global n) filters remote
 // sends so a remote vertex is sent once per improvement of its tentative depth.
 struct BfsPartApp {
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = false;
   uint32_t* dist;
   uint32_t* done;
@@ -97,7 +96,6 @@ struct BfsPartApp {
 // (global n, fp32) and are flushed as messages at the end of every round.
 template <class R>
 struct PrPartAppT {
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = false;
   double* rank;
   R* res;
@@ -150,7 +148,6 @@ struct PrPartAppT {
 // PR residue seeding on a partition (R4): local targets add to res, remote to racc.
 template <class R>
 struct PrPartInitAppT {
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = false;
   R* res;
   float* racc;
@@ -324,7 +321,7 @@ static atos_status part_ctx(atos_graph g, LaunchCtx& c) {
   c.g = g;
   c.cfg = g->dist->cfg;
   c.s = reinterpret_cast<cudaStream_t>(c.cfg.stream);
-  c.gv = GraphView{g->d_off, g->d_col, g->n};
+  c.gv = GraphView{g->d_off, g->d_col, g->n, g->col_cap};
   c.t0 = std::chrono::steady_clock::now();
   return ATOS_OK;
 }

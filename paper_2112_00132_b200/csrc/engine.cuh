@@ -25,6 +25,7 @@ struct GraphView {
   const int64_t* off;
   const int32_t* col;
   int64_t n;
+  int64_t col_cap;  // readable elements of col (>= m; TMA staging may read up to 3 past a list's end)
 };
 
 // ------------------------------------------------------------------ apps ---
@@ -33,10 +34,6 @@ struct GraphView {
 // per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
 // (strict, R2).
 struct BfsApp {
-  // CTA-local continuation (cta_ws2.cuh) measured slower on the 4899^2 grid
-  // (169 vs 93 ms: kept items wait in the CTA's batch pipeline) and 6.8x
-  // overwork on the road-like grid, so it is off for every app.
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   uint32_t* dist;
@@ -125,7 +122,6 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 
 template <class R>
 struct PrAppT {
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   double* rank;
@@ -184,7 +180,6 @@ struct PrAppT {
 // last completed task — a clean full sweep over unchanging residues.
 template <class R>
 struct PrWindowAppT {
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = true;
   double* rank;
   R* res;
@@ -237,7 +232,6 @@ struct PrWindowAppT {
 // but the frontier is rebuilt by the filter kernel, so nothing is appended.
 template <class R>
 struct PrBspAppT {
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   PrAppT<R> base;
@@ -443,7 +437,8 @@ __device__ __forceinline__ const Queue* chunk_queue(const RingSrc& s) { return s
 template <class App, class Sink, int U = LBS_UNROLL>
 __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g, const Sink& sink, const int64_t* pre,
                                              const int64_t* e0s, const typename App::Payload* pay, int n,
-                                             int64_t total, int64_t eb, int hint_lo = -1, int hint_hi = -1) {
+                                             int64_t total, int64_t eb, int hint_lo = -1, int hint_hi = -1,
+                                             const int* sofs = nullptr, const int32_t* stage = nullptr) {
   const int lane = lane_id();
   int lo, hi;
   if (hint_lo >= 0) {
@@ -457,6 +452,9 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
     lo = __shfl_sync(FULL_MASK, bound, 0);
     hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
   }
+#ifdef ATOS_STEP_PROF
+  const long long sp0 = clock64();
+#endif
   uint32_t w[U];
   int idx[U];
 #pragma unroll
@@ -467,27 +465,65 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
     if (e < total) {
       lo = lbs_find_range(pre, lo, hi, e);
       idx[k] = lo;
-      w[k] = (uint32_t)ld_stream_s32(g.col + e0s[lo] + (e - pre[lo]));
+      const int so = sofs ? sofs[lo] : -1;  // staged in shared memory by the agent's TMA copy?
+      w[k] = so >= 0 ? (uint32_t)stage[so + (int)(e - pre[lo])]
+                     : (uint32_t)ld_stream_s32(g.col + e0s[lo] + (e - pre[lo]));
     }
   }
+#ifdef ATOS_STEP_PROF
+  long long sp1;
+  {
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) x ^= w[k];
+    asm volatile("{ .reg .u32 t; add.u32 t, %1, 0; mov.u64 %0, %%clock64; }" : "=l"(sp1) : "r"(x));
+  }
+#endif
+  // (value-initialised: an uninitialised raw[k] on lanes without an edge made
+  // the compiler carry it across steps through local memory — an LDL/STL
+  // pair around every atomic)
   typename App::Probe pr[U];
 #pragma unroll
-  for (int k = 0; k < U; ++k)
+  for (int k = 0; k < U; ++k) {
+    pr[k] = typename App::Probe{};
     if (idx[k] >= 0) pr[k] = app.probe(w[k]);
+  }
   typename App::Raw raw[U];
   typename App::Payload pk[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) {
+    raw[k] = typename App::Raw{};
     pk[k] = idx[k] >= 0 ? pay[idx[k]] : typename App::Payload{};
     if (idx[k] >= 0) raw[k] = app.issue(pk[k], w[k], pr[k]);
   }
   bool act[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) act[k] = idx[k] >= 0 && app.decide(pk[k], w[k], pr[k], raw[k]);
+#ifdef ATOS_STEP_PROF
+  long long sp2;
+  {
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) x += act[k];
+    asm volatile("{ .reg .u32 t; add.u32 t, %1, 0; mov.u64 %0, %%clock64; }" : "=l"(sp2) : "r"(x));
+  }
+#endif
   uint32_t item[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) item[k] = app.item_of(w[k]);
+#ifdef ATOS_STEP_PROF
+  const uint32_t pushed_ = sink.template warp_push_multi<U>(act, item);
+  const long long sp3 = clock64();
+  if (lane == 0 && sink.q.ctl) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[6].v), (unsigned long long)(sp1 - sp0));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[7].v), (unsigned long long)(sp2 - sp1));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[8].v), (unsigned long long)(sp3 - sp2));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[9].v), 1ull);
+  }
+  return pushed_;
+#else
   return sink.template warp_push_multi<U>(act, item);
+#endif
 }
 
 template <class App, class Sink>

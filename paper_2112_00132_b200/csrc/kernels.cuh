@@ -23,7 +23,7 @@ struct EdgeMapPolicy {
   static constexpr bool kWarpSpecialised = true;
   using Payload = typename App::Payload;
   static __host__ __device__ size_t smem_bytes(int F) { return cta_smem_bytes<Payload>(F); }
-  static __host__ __device__ size_t ws_smem(int F) { return ws2_smem_bytes<Payload>(F); }
+  static __host__ __device__ size_t ws_smem(int F, int S) { return ws2_smem_bytes<Payload>(F, S); }
   static __device__ __forceinline__ void cta_persistent(const App& app, const GraphView& g, const Queue& q, int F,
                                                         unsigned char* smem, LocalStats& st) {
     cta_ws2_persistent(app, g, q, F, smem, st);
@@ -50,7 +50,7 @@ template <int MODE>
 struct GcPolicy {
   static constexpr bool kSplit = false;
   static constexpr bool kWarpSpecialised = false;
-  static __host__ __device__ size_t ws_smem(int) { return 0; }
+  static __host__ __device__ size_t ws_smem(int, int) { return 0; }
   static __device__ __forceinline__ void cta_persistent(const GcApp&, const GraphView&, const Queue&, int,
                                                         unsigned char*, LocalStats&) {}
   static __host__ __device__ size_t smem_bytes(int F) { return gc_cta_smem_bytes(F); }
@@ -116,8 +116,8 @@ struct StageSrc {
 
 // dynamic shared memory per block for a worker kind
 template <class P>
-__host__ __device__ inline size_t worker_smem_bytes(int W, int F, int T, bool persistent = false) {
-  if (W == W_CTA) return (persistent && P::kWarpSpecialised) ? P::ws_smem(F) : P::smem_bytes(F);
+__host__ __device__ inline size_t worker_smem_bytes(int W, int F, int T, bool persistent = false, int S = 0) {
+  if (W == W_CTA) return (persistent && P::kWarpSpecialised) ? P::ws_smem(F, S) : P::smem_bytes(F);
   if (W == W_WARP) return (size_t)(T / 32) * (size_t)F * 4;
   return (size_t)T * (size_t)F * 4;
 }
@@ -354,7 +354,6 @@ __global__ void k_ctl_init(QueueCtl* ctl, uint64_t tail, uint64_t* ring, int64_t
   ctl->chunk_tail.v = 0;
   ctl->chunk_done.v = 0;
   ctl->trace_count.v = 0;
-  ctl->kept.v = 0;
   for (int i = 0; i < 4; ++i) { ctl->stats[i].v = 0; ctl->aux[i].v = 0; }
   if (src_item >= 0) ring[0] = (1ull << 32) | (uint64_t)(uint32_t)src_item;
 }
@@ -372,7 +371,6 @@ __global__ void k_bfs_init(uint32_t* dist, uint32_t* done, uint16_t* near, int64
 // app that pushes c = (1-a) a / deg(v) to every out-neighbour, no activation.
 template <class R>
 struct PrInitAppT {
-  static constexpr bool kKeep = false;
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   R* res;

@@ -1,0 +1,16 @@
+"""Build a tuning variant of libatos.so with extra -D flags (experiments only).
+
+usage: python tools/build_variant.py TAG -DFOO=1 ...  ->  paper_2112_00132_b200/variants/libatos_TAG.so
+Run a variant with tools/libswap.sh <so> <command>.
+"""
+import os, subprocess, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2112_00132_b200 import build as b
+
+tag, flags = sys.argv[1], sys.argv[2:]
+out_dir = os.path.join(b.HERE, "variants")
+os.makedirs(out_dir, exist_ok=True)
+out = os.path.join(out_dir, f"libatos_{tag}.so")
+cmd = [b.nvcc(), *b.NVCC_FLAGS, *flags, "-I", os.path.join(b.ROOT, "include"), "-o", out, *b.sources(), "-ldl"]
+subprocess.check_call(cmd)
+print(out)

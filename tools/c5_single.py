@@ -1,0 +1,51 @@
+"""C5 (BASELINE configs[4]) on ONE B200: RMAT-27 (134M vertices, ~2.1B arcs), BFS from 0 and
+PageRank (alpha=0.85, eps=1e-6) through the C ABI; BFS checked bit-exact against the serial
+oracle (test infrastructure).  Prints one JSON line.  Not part of the product path."""
+import argparse, json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import graphgen as gg
+import paper_2112_00132_b200 as atos
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--scale", type=int, default=27)
+ap.add_argument("--runs", type=int, default=3)
+ap.add_argument("--pr-runs", type=int, default=1)
+ap.add_argument("--no-oracle", action="store_true")
+a = ap.parse_args()
+t = time.time()
+g = gg.rmat(a.scale, 16, seed=1)
+gen_s = time.time() - t
+print(f"generated n={g.n} m={g.m} in {gen_s:.1f}s", flush=True)
+G = atos.Graph(g.off, g.col)
+dev = torch.device("cuda", 0)
+depth = torch.empty(g.n, dtype=torch.int32, device=dev)
+rank_out = torch.empty(g.n, dtype=torch.float32, device=dev)
+cfg_bfs = atos.Config(fetch_size=128, cta_threads=256, timeout_s=300)
+cfg_pr = atos.Config(fetch_size=128, cta_threads=512, timeout_s=600)
+flush = torch.empty(512 << 18, dtype=torch.float32, device=dev)
+bfs_ms, pr_ms, pr_pushes = [], [], []
+for i in range(a.runs + 1):
+    flush.fill_(1.0); torch.cuda.synchronize()
+    _, st = atos.bfs(G, 0, cfg_bfs, out=depth)
+    if i: bfs_ms.append(st["ms"])
+for i in range(a.pr_runs):
+    flush.fill_(1.0); torch.cuda.synchronize()
+    _, sp = atos.pagerank(G, 0.85, 1e-6, cfg_pr, out=rank_out)
+    pr_ms.append(sp["ms"]); pr_pushes.append(sp["edges_processed"])
+d = depth.cpu().numpy().view(np.uint32)
+deg = g.degrees()
+reached = d != atos.UNREACHED
+e_bfs = int(deg[reached].sum())
+out = {"workload": f"rmat{a.scale}_ef16 single GPU (C5 at N=1)", "n": g.n, "m": g.m, "gen_s": round(gen_s, 1),
+       "bfs": {"ms_median": float(np.median(bfs_ms)), "ms_all": bfs_ms, "edges": e_bfs, "reached": int(reached.sum()),
+               "gteps": e_bfs / (np.median(bfs_ms) * 1e-3) / 1e9, "overwork": st["tasks_popped"] / max(1, int(reached.sum()))},
+       "pagerank": {"ms": pr_ms, "edge_pushes": pr_pushes, "gteps_raw": pr_pushes[0] / (pr_ms[0] * 1e-3) / 1e9,
+                    "max_residue": sp["max_residue"], "pops": sp["tasks_popped"]}}
+if not a.no_oracle:
+    import oracle
+    t = time.time()
+    ref = oracle.bfs(g, 0)
+    out["bfs"]["oracle_s"] = round(time.time() - t, 1)
+    out["bfs"]["bit_exact_vs_oracle"] = bool(np.array_equal(ref, d))
+print(json.dumps(out), flush=True)
