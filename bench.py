@@ -65,6 +65,11 @@ def parse():
     return ap.parse_args()
 
 
+# returning f32 atomicAdd on random addresses of a 64 MB array, all SMs (profiles/r01_ubench.txt)
+ATOM_SKEWED_GOPS = 103.6
+ATOM_UNIFORM_GOPS = 128.2
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -272,6 +277,14 @@ def run_atos(args, rank, world, local_rank):
                      "traffic_source": "profiles/r01_traffic.json (ncu --set full, same config)",
                      "algorithmic_bytes": pr_bytes, "kernel": "k_persistent<PrAppT<float>, CTA>",
                      "bytes_model": "8 B/edge push + 32 B/pop", "peak_kind": peak_kind},
+        # PageRank's edge push is one returning fp32 atomicAdd at L2 on a random, RMAT-skewed address:
+        # the ceiling it actually runs against is the L2 atomic rate measured by tools/ubench.cu
+        "atomic_ceiling": {"achieved_gops": statistics.mean(e / (k * 1e-3) / 1e9 for e, k in
+                                                            zip(e_pr, (r[3]["kernel_ms"] for r in records))),
+                           "peak_gops": ATOM_SKEWED_GOPS, "peak_uniform_gops": ATOM_UNIFORM_GOPS,
+                           "frac": statistics.mean(e / (k * 1e-3) / 1e9 for e, k in
+                                                   zip(e_pr, (r[3]["kernel_ms"] for r in records))) / ATOM_SKEWED_GOPS,
+                           "source": "profiles/r01_ubench.txt (returning f32 atomicAdd, RMAT-like skew / uniform)"},
         "bfs": {"gteps": e_bfs / (statistics.mean(t_bfs) * 1e-3) / 1e9, "ms": statistics.mean(t_bfs),
                 "kernel_ms": bfs_kms, "edges": e_bfs, "reached": v_bfs,
                 "roofline_frac": bfs_ach / hbm, "achieved_gbs": bfs_ach,
@@ -379,6 +392,8 @@ def run_atos_multi(args, rank, world, local_rank):
                         recs[-1][4]["rounds"], sum(r[3]["bytes_sent"] + r[4]["bytes_sent"] for r in recs)],
                        dtype=torch.float64, device=dev)
     dist.all_reduce(loc)
+    # this rank's kernel launches per step (the library counts every launch it makes)
+    launches = sum(r[3]["kernel_launches"] + r[4]["kernel_launches"] for r in recs) // len(recs)
     e_bfs, e_pr = int(loc[0].item()), float(loc[1].item())
     tot_ms = float(t[0].item())
     value = (e_bfs * len(recs) + e_pr) / (tot_ms * 1e-3) / 1e9
@@ -402,7 +417,7 @@ def run_atos_multi(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": (8.0 * e_pr / len(recs)) / (float(t[2].item()) / len(recs) * 1e-3) / 1e9 / world,
                      "peak": hbm, "unit": "GB/s", "frac": None, "traffic": None, "peak_kind": peak_kind,
                      "note": "per-GPU average of the PageRank edge-push bytes over the whole multi-round step"},
-        "gpu_launches": None,
+        "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     out["roofline"]["frac"] = out["roofline"]["achieved"] / hbm

@@ -78,7 +78,8 @@ typedef struct {
   void* trace;            /* optional device buffer of atos_trace_rec (timeline);  */
   int64_t trace_capacity; /*   records; one per processed batch; extra records are dropped    */
   int32_t stage_edges;    /* persistent CTA workers: column-list staging per batch buffer via   */
-                          /*   TMA bulk copies, in edges; -1 = auto, 0 = off       */
+                          /*   TMA bulk copies, in edges; 0 = off (default), -1 =   */
+                          /*   auto (largest that keeps occupancy and 64 KB of L1 per SM)       */
   int32_t _pad0;
 } atos_config;
 

@@ -137,7 +137,7 @@ class Config:
     timeout_s: float = 60.0
     stream: int | None = None      # raw cudaStream_t; None = torch current stream
     trace: object = None           # Trace() buffer for the timeline, or None
-    stage_edges: int = -1          # TMA column staging per batch buffer (edges); -1 auto, 0 off
+    stage_edges: int = 0           # TMA column staging per batch buffer (edges); 0 off, -1 auto
 
     def to_c(self) -> CConfig:
         c = CConfig()

@@ -189,6 +189,48 @@ def test_bfs_device_output_and_torch_borrow(atos):
     assert np.array_equal(d.cpu().numpy().view(np.uint32), oracle.bfs(g, 3))
 
 
+@pytest.mark.parametrize("stage", [0, 256, 1024, 8192])
+@pytest.mark.parametrize("gname,src", [("rmat16", 0), ("hub", 0), ("road", 17), ("star", 3)])
+def test_bfs_column_staging(atos, gname, src, stage):
+    """Persistent CTA workers with TMA-staged column lists: every
+    staging capacity (0 = off, 256 = most items fall back to global loads,
+    8192 = whole batches staged) gives the oracle's depths."""
+    for fetch, thr in [(128, 256), (7, 64), (1024, 512)]:
+        d, _ = atos.bfs(D(atos, gname), src, fetch_size=fetch, cta_threads=thr, stage_edges=stage)
+        assert np.array_equal(d, oracle.bfs(G(gname), src)), (fetch, thr)
+
+
+def test_staging_borrowed_unpadded_columns(atos):
+    """A borrowed column array has no padding: the list ending at m must not be
+    bulk-copied past the allocation (it falls back to global loads)."""
+    import torch
+    g = gg.from_edges(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (5, 1)])  # m = 7: last list ends at m
+    assert g.m % 4 != 0
+    off = torch.from_numpy(g.off).cuda()
+    col = torch.from_numpy(g.col[:]).cuda()
+    Gt = atos.Graph(off, col)
+    d, _ = atos.bfs(Gt, 0, stage_edges=1024)
+    assert np.array_equal(d, oracle.bfs(g, 0))
+    x = oracle.pagerank(g, 0.85)[0]
+    r, st = atos.pagerank(Gt, 0.85, 1e-6, stage_edges=1024)
+    assert np.max(np.abs(r - x)) / x.max() <= PR_TOL
+
+
+@pytest.mark.parametrize("stage", [0, 512, 4096])
+def test_pagerank_column_staging(atos, stage):
+    x = jacobi("rmat16")
+    for fetch, thr in [(128, 512), (16, 128)]:
+        r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, fetch_size=fetch, cta_threads=thr, stage_edges=stage)
+        assert np.max(np.abs(r - x)) / x.max() <= PR_TOL
+        assert st["max_residue"] <= 1e-6
+
+
+def test_stage_edges_invalid(atos):
+    with pytest.raises(atos.AtosError) as e:
+        atos.bfs(D(atos, "K9"), 0, stage_edges=-2)
+    assert e.value.name == "INVALID_ARGUMENT"
+
+
 def test_bfs_queue_wraparound(atos):
     g = G("grid64")
     d, st = atos.bfs(D(atos, "grid64"), 0, queue_capacity=256, worker="warp", fetch_size=4)
