@@ -172,7 +172,13 @@ const char* atos_version(void);
  * BFS: a remote vertex is sent at most once per improvement (per-rank
  * sent_min filter).  PageRank: remote contributions are accumulated per
  * destination vertex; a round sends those above eps, and the run closes with
- * a flush-all round (no mass is stranded).  Colouring is single-GPU (replicas only). */
+ * a flush-all round (no mass is stranded).  Colouring (app 2, SURVEY §8f row
+ * f4; needs ATOS_GRAPH_SYMMETRIC, world <= 64): each rank colours its vertices
+ * with Alg. 6 against a replica of all colours; a message is
+ * (uint64)(global_id << 32 | colour), sent once per round to every rank owning
+ * a neighbour of a vertex whose colour changed; the receiver re-ASSIGNs a
+ * local v that now shares a colour with a smaller changed neighbour (R13 across
+ * ranks).  The run ends after a round in which no rank sent anything. */
 
 /* Partitioned graph for rank `rank` of `world`: it owns global vertices
  * [bounds[rank], bounds[rank+1]) (bounds: host int64[world+1], bounds[0] = 0,
@@ -184,8 +190,9 @@ atos_status atos_graph_create_partitioned(int64_t global_n, int32_t world, int32
                                           const int32_t* col_global, int64_t local_m, uint32_t flags,
                                           atos_graph* out);
 /* Start a partitioned run: app 0 = BFS from global vertex src (alpha/eps
- * ignored), app 1 = PageRank(alpha, eps) (src ignored).  Initialises local
- * state (timed into the first round's stats). */
+ * ignored), app 1 = PageRank(alpha, eps) (src ignored), app 2 = greedy
+ * colouring (src/alpha/eps ignored; INVALID_GRAPH without SYMMETRIC).
+ * Initialises local state (timed into the first round's stats). */
 atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, float alpha, float eps,
                             const atos_config* cfg);
 /* One exchange round: run the local queue kernel — persistent: to local
@@ -201,9 +208,10 @@ atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* send_counts)
 atos_status atos_part_pack(atos_graph g, uint64_t* dst, int64_t cap);
 /* Apply received messages (host or device buffer of `count` uint64):
  * BFS atomicMin + push on improvement; PageRank atomicAdd + push on an
- * eps crossing. */
+ * eps crossing; colouring: ghost colour update, then every local vertex in
+ * conflict with a smaller changed ghost is re-ASSIGNed. */
 atos_status atos_part_apply(atos_graph g, const uint64_t* msgs, int64_t count);
-/* Finish: write the local results (BFS: uint32 depth, PageRank: float rank;
+/* Finish: write the local results (BFS: uint32 depth, PageRank: float rank, colouring: int32 colour;
  * n_local = bounds[rank+1]-bounds[rank] entries, host or device) and the
  * accumulated statistics (rounds = exchange rounds; bytes_sent = message bytes). */
 atos_status atos_part_finish(atos_graph g, void* out, atos_stats* stats);

@@ -853,7 +853,7 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
                                   atos_stats* st) {
   LaunchCtx c;
   CKS(begin_call(g, cfg, c, st));
-  if (g->dist) return atos_set_error(ATOS_ERR_UNSUPPORTED, "colouring is single-GPU (SURVEY §8e: replicas only)");
+  if (g->dist) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "partitioned graph: use atos_part_begin(app = 2)");
   if (!g->symmetric) return atos_set_error(ATOS_ERR_INVALID_GRAPH, "atos_color needs ATOS_GRAPH_SYMMETRIC");
   if (c.cfg.gc_literal) return atos_set_error(ATOS_ERR_UNSUPPORTED, "paper-literal colouring (livelocks, R13) not built");
   const int64_t n = g->n;

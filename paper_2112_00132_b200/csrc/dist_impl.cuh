@@ -226,6 +226,88 @@ __global__ void k_part_apply(const uint64_t* msgs, int64_t count, uint32_t* dist
   }
 }
 
+// ------------------------------------------------ partitioned colouring (f4)
+// Round structure: every rank runs the uberkernel (Alg. 6)
+// on its own vertices to local quiescence, reading neighbours' colours from a
+// replica of all N colours (ghost entries as last received).  At the round's
+// end each vertex whose colour changed sends (global id, colour) once to every
+// other rank owning one of its neighbours; the receiver updates its replica
+// and re-checks its vertices against the changed ghosts: a local v whose
+// colour equals a changed neighbour u's and v > u is re-ASSIGNed (R13 across
+// ranks: the larger endpoint recolours, so the smallest id in a conflict
+// never moves and the rounds terminate).  A cut edge left monochromatic would
+// need its larger endpoint's owner to have missed the other endpoint's last
+// change, which every change is sent to — so the final colouring is proper.
+
+// One warp per changed local vertex: the set of remote owners of its
+// neighbours (columns are sorted global ids; owners are a 64-bit mask, world
+// <= 64) gets one message (vg << 32 | colour) each.
+__global__ void k_gc_pack(const GraphView g, const int32_t* color, uint8_t* chg, uint32_t vb, const int64_t* bounds,
+                          int world, int rank, Outbox out) {
+  const int lane = lane_id();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t base = warp * 32; base < g.n; base += nwarps * 32) {
+    const int64_t my = base + lane;
+    const bool c = my < g.n && chg[my];
+    unsigned todo = __ballot_sync(FULL_MASK, c);
+    if (c) chg[my] = 0;
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t v = (uint32_t)(base + j);
+      const int64_t e0 = ld_nc_s64(g.off + v), e1 = ld_nc_s64(g.off + v + 1);
+      unsigned long long mask = 0;
+      for (int64_t e = e0 + lane; e < e1; e += 32) {
+        const int r = owner_of(bounds, world, (uint32_t)g.col[e]);
+        if (r != rank) mask |= 1ull << r;
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) mask |= __shfl_xor_sync(FULL_MASK, mask, d);
+      const uint32_t c_v = (uint32_t)ld_relaxed_s32(color + vb + v);
+      const unsigned long long msg = ((unsigned long long)(vb + v) << 32) | c_v;
+      for (int r = lane; r < world; r += 32)
+        if ((mask >> r) & 1ull) out.put(r, msg);
+    }
+  }
+}
+
+// Received ghost colours: replica update + changed-ghost mark.
+__global__ void k_gc_apply(const uint64_t* msgs, int64_t count, int32_t* color, uint8_t* gchg, uint8_t val) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t m = msgs[i];
+    const uint32_t u = (uint32_t)(m >> 32);
+    if (val) color[u] = (int32_t)(uint32_t)m;
+    gchg[u] = val;
+  }
+}
+
+// Re-check every local vertex against the ghosts that changed this round
+// (warp per vertex): a conflict with a smaller changed ghost re-ASSIGNs v
+// (pend dedupe, as a local CHECK would).
+__global__ void k_gc_ghost_scan(const GraphView g, const int32_t* color, const uint8_t* gchg, uint32_t* pend,
+                                uint32_t vb, Queue q) {
+  const int lane = lane_id();
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < g.n; v += nwarps) {
+    const uint32_t vg = vb + (uint32_t)v;
+    const int64_t e0 = ld_nc_s64(g.off + v), e1 = ld_nc_s64(g.off + v + 1);
+    const int32_t cv = ld_relaxed_s32(color + vg);
+    bool hit = false;
+    for (int64_t e = e0 + lane; e < e1 && !hit; e += 32) {
+      const uint32_t u = (uint32_t)g.col[e];
+      hit = u < vg && gchg[u] && color[u] == cv;
+    }
+    hit = __any_sync(FULL_MASK, hit);
+    bool act = false;
+    if (hit && lane == 0) {
+      __threadfence();
+      act = atomicExch(pend + v, 1u) == 0u;
+    }
+    q_warp_push(q, act, (uint32_t)v);
+  }
+}
+
 }  // namespace atos
 
 struct DistState {
@@ -239,6 +321,9 @@ struct DistState {
   unsigned long long* h_cnt = nullptr;  // pinned
   uint32_t* sent_min = nullptr;
   float* racc = nullptr;
+  int32_t* gc_color = nullptr;  // colouring: replica of all N colours
+  uint8_t* gc_chg = nullptr;    // colouring: local vertex changed colour this round
+  uint8_t* gc_gchg = nullptr;   // colouring: ghost changed this round (global ids)
   int app = -1;
   float alpha = 0.85f, eps = 1e-6f;
   atos_config cfg{};
@@ -258,6 +343,9 @@ void dist_free(atos_graph g) {
   if (d->h_cnt) cudaFreeHost(d->h_cnt);
   cudaFree(d->sent_min);
   cudaFree(d->racc);
+  cudaFree(d->gc_color);
+  cudaFree(d->gc_chg);
+  cudaFree(d->gc_gchg);
   delete d;
   g->dist = nullptr;
 }
@@ -332,7 +420,13 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
   CKS(begin_call(g, cfg, c, nullptr));
   if (!g->dist) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "not a partitioned graph");
   DistState* d = g->dist;
-  if (app != 0 && app != 1) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "app must be 0 (BFS) or 1 (PageRank)");
+  if (app < 0 || app > 2)
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "app must be 0 (BFS), 1 (PageRank) or 2 (colouring)");
+  if (app == 2 && !g->symmetric)
+    return atos_set_error(ATOS_ERR_INVALID_GRAPH, "partitioned colouring needs ATOS_GRAPH_SYMMETRIC");
+  if (app == 2 && d->world > 64) return atos_set_error(ATOS_ERR_UNSUPPORTED, "partitioned colouring: world > 64");
+  if (app == 2 && c.cfg.worker != ATOS_WORKER_CTA && c.cfg.worker != ATOS_WORKER_WARP && c.cfg.worker != ATOS_WORKER_THREAD)
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "bad worker");
   if (app == 0 && (src < 0 || src >= g->global_n)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "src out of range");
   if (app == 1 && (!(alpha > 0.f && alpha < 1.f) || !(eps > 0.f)))
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "alpha/eps");
@@ -348,8 +442,8 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
   d->r64 = c.cfg.pr_residue_fp64 != 0;
   const int64_t n = g->n, N = g->global_n;
   Workspace& w = g->ws;
-  CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)std::max<int64_t>(n, 1), true, c.s));
-  if (app == 1 && (uint64_t)n > w.cap) return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "queue_capacity < n");
+  CKS(ws_prepare(g, c.cfg, n, (app == 2 ? 4 : 2) * (uint64_t)std::max<int64_t>(n, 1), true, c.s));
+  if (app >= 1 && (uint64_t)n > w.cap) return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "queue_capacity < n");
   CK(cudaMemsetAsync(d->d_cnt, 0, (d->world + 1) * sizeof(unsigned long long), c.s));
   CK(cudaEventRecord(w.ev[0], c.s));
   if (app == 0) {
@@ -362,6 +456,21 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
     k_fill<uint32_t><<<fill_blocks(N, g->sms), 256, 0, c.s>>>(d->sent_min, N, 0xFFFFFFFFu);
     k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, mine ? 1 : 0, w.ring, mine ? src - g->v_begin : -1);
     d->launches += 3;
+  } else if (app == 2) {
+    // colouring: replica colours -1, pend = 1 (every vertex has its initial ASSIGN queued), ASSIGN(v) in id order
+    CKS(ensure(w.u32a, w.u32a_n, (size_t)std::max<int64_t>(n, 1)));
+    if (!d->gc_color) CK(cudaMalloc(&d->gc_color, (size_t)std::max<int64_t>(N, 1) * sizeof(int32_t)));
+    if (!d->gc_gchg) {
+      CK(cudaMalloc(&d->gc_gchg, (size_t)std::max<int64_t>(N, 1)));
+      CK(cudaMemsetAsync(d->gc_gchg, 0, (size_t)std::max<int64_t>(N, 1), c.s));
+    }
+    if (!d->gc_chg) CK(cudaMalloc(&d->gc_chg, (size_t)std::max<int64_t>(n, 1)));
+    CK(cudaMemsetAsync(d->gc_chg, 0, (size_t)std::max<int64_t>(n, 1), c.s));
+    k_fill<int32_t><<<fill_blocks(std::max<int64_t>(N, 1), g->sms), 256, 0, c.s>>>(d->gc_color, N, -1);
+    k_fill<uint32_t><<<fill_blocks(std::max<int64_t>(n, 1), g->sms), 256, 0, c.s>>>(w.u32a, n, 1u);
+    k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, (uint64_t)n, w.ring, -1);
+    if (n) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
+    d->launches += 4;
   } else {
     CKS(ensure(w.f32a, w.f32a_n, (size_t)std::max<int64_t>(n, 1)));
     CKS(ensure(w.f64a, w.f64a_n, (size_t)std::max<int64_t>(n, 1)));
@@ -418,7 +527,16 @@ extern "C" atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* s
     if (disc) return run_discrete<EdgeMapPolicy<A>>(c, app, q, tail_now, d->next_h, 1, &d->next_h);
     return run_persistent<EdgeMapPolicy<A>>(c, app, q);
   };
-  if (d->app == 0) {
+  if (d->app == 2) {
+    GcApp app{d->gc_color, w.u32a, vb, ve, d->gc_chg};
+    if (disc) CKS(run_discrete<GcPolicy<GC_UBER>>(c, app, q, tail_now, d->next_h, 1, &d->next_h));
+    else CKS(run_persistent<GcPolicy<GC_UBER>>(c, app, q));
+    if (g->n) {
+      k_gc_pack<<<fill_blocks(g->n, g->sms), 256, 0, c.s>>>(c.gv, d->gc_color, d->gc_chg, vb, d->d_bounds, d->world,
+                                                             d->rank, ob);
+      c.launches++;
+    }
+  } else if (d->app == 0) {
     CKS(go(BfsPartApp{w.u32a, w.u32b, d->sent_min, c.cfg.bfs_filter, vb, ve, d->d_bounds, d->world, ob}));
   } else if (d->r64) {
     CKS(go(PrPartAppT<double>{w.f64a, w.f64b, (double)d->alpha, (double)d->eps, vb, ve, d->racc}));
@@ -502,11 +620,18 @@ extern "C" atos_status atos_part_apply(atos_graph g, const uint64_t* msgs, int64
   Queue q = make_queue(g, c.cfg, (uint32_t)d->app);
   q.deadline = 0;
   const int blocks = fill_blocks(count, g->sms);
-  if (d->app == 0) k_part_apply<0, float><<<blocks, 256, 0, c.s>>>(dm, count, w.u32a, (float*)nullptr, 0.f, q);
+  if (d->app == 2) {
+    k_gc_apply<<<blocks, 256, 0, c.s>>>(dm, count, d->gc_color, d->gc_gchg, 1);
+    if (g->n)
+      k_gc_ghost_scan<<<fill_blocks(g->n * 32, g->sms), 256, 0, c.s>>>(c.gv, d->gc_color, d->gc_gchg, w.u32a,
+                                                                        (uint32_t)g->v_begin, q);
+    k_gc_apply<<<blocks, 256, 0, c.s>>>(dm, count, nullptr, d->gc_gchg, 0);
+    d->launches += g->n ? 3 : 2;
+  } else if (d->app == 0) k_part_apply<0, float><<<blocks, 256, 0, c.s>>>(dm, count, w.u32a, (float*)nullptr, 0.f, q);
   else if (d->r64) k_part_apply<1, double><<<blocks, 256, 0, c.s>>>(dm, count, nullptr, w.f64b, (double)d->eps, q);
   else k_part_apply<1, float><<<blocks, 256, 0, c.s>>>(dm, count, nullptr, w.f32b, d->eps, q);
   CK(cudaGetLastError());
-  d->launches++;
+  if (d->app != 2) d->launches++;
   if (tmp) CK(cudaFreeAsync(tmp, c.s));
   CKS(read_ctl(g, c.s));
   return ATOS_OK;
@@ -524,6 +649,8 @@ extern "C" atos_status atos_part_finish(atos_graph g, void* out, atos_stats* st)
   if (n) {
     if (d->app == 0) {
       CKS(copy_out(out, w.u32a, (size_t)n * sizeof(uint32_t), c.s));
+    } else if (d->app == 2) {
+      CKS(copy_out(out, d->gc_color + g->v_begin, (size_t)n * sizeof(int32_t), c.s));
     } else {
       k_f64_to_f32<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.f64a, w.f32a, n);
       CK(cudaGetLastError());

@@ -23,9 +23,22 @@
 
 namespace atos {
 
+// Queue items and pend[] are LOCAL vertex ids; colours are indexed by GLOBAL
+// id (v + vb).  On one GPU vb = 0 and the range is everything.  On a 1-D
+// partition `color` is this rank's replica of all N
+// colours (owned entries authoritative, ghosts as last received), a conflict
+// whose larger endpoint is remote is left to its owner, and every ASSIGN
+// marks chg[v] so the round's end sends the new colour to the neighbours'
+// owners (dist_impl.cuh).
 struct GcApp {
   int32_t* color;
   uint32_t* pend;
+  uint32_t vb = 0, ve = 0xFFFFFFFFu;  // owned global ids [vb, ve)
+  uint8_t* chg = nullptr;             // partitioned runs: colour changed this round (local ids)
+  __device__ __forceinline__ bool owned(uint32_t u) const { return u >= vb && u < ve; }
+  __device__ __forceinline__ void assigned(uint32_t v) const {
+    if (chg) chg[v] = 1;
+  }
 };
 
 enum GcMode : int { GC_UBER = 0, GC_BSP_ASSIGN = 1, GC_BSP_DETECT = 2 };
@@ -85,7 +98,7 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
       sm.e0[i] = ld_nc_s64(g.off + v);
       sm.pre[i] = ld_nc_s64(g.off + v + 1) - sm.e0[i];
       if (t & GC_CHECK_BIT) {
-        sm.col_v[i] = ld_relaxed_s32(app.color + v);
+        sm.col_v[i] = ld_relaxed_s32(app.color + app.vb + v);
       } else {
         if (MODE == GC_UBER) { atomicExch(app.pend + v, 0u); fenced = true; }
         sm.col_v[i] = 0;  // window base
@@ -113,7 +126,7 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
       if (e < total) {
         const int i = lbs_find(sm.pre, (int)n, e);
         const uint32_t t = sm.task[i];
-        const uint32_t v = t & ~GC_CHECK_BIT;
+        const uint32_t v = (t & ~GC_CHECK_BIT) + app.vb;  // global id
         const uint32_t u = (uint32_t)ld_stream_s32(g.col + sm.e0[i] + (e - sm.pre[i]));
         if (u != v) {
           const int32_t cu = ld_relaxed_s32(app.color + u);
@@ -123,9 +136,9 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
                 if (u < v) sm.flag[i] = 1;
               } else if (u < v) {
                 sm.flag[i] = 1;  // v itself must recolour (one push per task, R12)
-              } else {
+              } else if (app.owned(u)) {  // a remote larger endpoint is its owner's to recolour
                 __threadfence();
-                if (atomicExch(app.pend + u, 1u) == 0u) { act = true; push_item = u; }
+                if (atomicExch(app.pend + (u - app.vb), 1u) == 0u) { act = true; push_item = u - app.vb; }
               }
             }
           } else {
@@ -149,7 +162,8 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
         const int f = gc_first_free(sm.bits + i * GC_WIN_WORDS);
         const uint32_t v = t;
         if (f >= 0) {
-          st_relaxed_s32(app.color + v, sm.col_v[i] + f);
+          st_relaxed_s32(app.color + app.vb + v, sm.col_v[i] + f);
+          app.assigned(v);
           stored = true;
           sm.flag[i] = 2;  // assigned in this batch
         } else {
@@ -206,11 +220,12 @@ template <int MODE, class Sink>
 __device__ __forceinline__ uint32_t gc_warp_task(const GcApp& app, const GraphView& g, const Sink& sink, uint32_t t,
                                                  uint64_t& edges) {
   const int lane = lane_id();
-  const uint32_t v = t & ~GC_CHECK_BIT;
+  const uint32_t v = t & ~GC_CHECK_BIT;  // local id
+  const uint32_t vg = v + app.vb;        // global id
   const int64_t e0 = ld_nc_s64(g.off + v), e1 = ld_nc_s64(g.off + v + 1);
   uint32_t pushed = 0;
   if (t & GC_CHECK_BIT) {
-    const int32_t c = ld_relaxed_s32(app.color + v);
+    const int32_t c = ld_relaxed_s32(app.color + vg);
     bool self = false;
     edges += e1 - e0;
     for (int64_t eb = e0; eb < e1; eb += 32) {
@@ -219,15 +234,15 @@ __device__ __forceinline__ uint32_t gc_warp_task(const GcApp& app, const GraphVi
       uint32_t u = 0;
       if (e < e1) {
         u = (uint32_t)ld_stream_s32(g.col + e);
-        if (u != v && ld_relaxed_s32(app.color + u) == c) {
-          if (u < v) self = true;
-          else if (MODE == GC_UBER) {
+        if (u != vg && ld_relaxed_s32(app.color + u) == c) {
+          if (u < vg) self = true;
+          else if (MODE == GC_UBER && app.owned(u)) {
             __threadfence();
-            act = atomicExch(app.pend + u, 1u) == 0u;
+            act = atomicExch(app.pend + (u - app.vb), 1u) == 0u;
           }
         }
       }
-      if (MODE == GC_UBER) pushed += sink.warp_push(act, u);
+      if (MODE == GC_UBER) pushed += sink.warp_push(act, u - app.vb);
     }
     self = __any_sync(FULL_MASK, self);
     bool act = false;
@@ -257,7 +272,7 @@ __device__ __forceinline__ uint32_t gc_warp_task(const GcApp& app, const GraphVi
     edges += e1 - e0;
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const uint32_t u = (uint32_t)ld_stream_s32(g.col + e);
-      if (u == v) continue;
+      if (u == vg) continue;
       const int32_t r = ld_relaxed_s32(app.color + u) - base;
       if (r >= 0 && r < 32 * GC_WIN_WORDS) {
 #pragma unroll
@@ -272,7 +287,8 @@ __device__ __forceinline__ uint32_t gc_warp_task(const GcApp& app, const GraphVi
   }
   bool act = false;
   if (lane == 0) {
-    st_relaxed_s32(app.color + v, chosen);
+    st_relaxed_s32(app.color + vg, chosen);
+    app.assigned(v);
     __threadfence();
     act = (MODE == GC_UBER);
   }
@@ -286,14 +302,15 @@ template <int MODE, class Sink>
 __device__ __forceinline__ uint32_t gc_thread_task(const GcApp& app, const GraphView& g, const Sink& sink,
                                                    bool valid, uint32_t t, uint64_t& edges) {
   uint32_t pushed = 0;
-  const uint32_t v = t & ~GC_CHECK_BIT;
+  const uint32_t v = t & ~GC_CHECK_BIT;  // local id
+  const uint32_t vg = v + app.vb;        // global id
   int64_t e0 = 0, e1 = 0;
   if (valid) { e0 = ld_nc_s64(g.off + v); e1 = ld_nc_s64(g.off + v + 1); }
   const bool is_check = valid && (t & GC_CHECK_BIT);
   const bool is_assign = valid && !(t & GC_CHECK_BIT);
   // CHECK
   {
-    const int32_t c = is_check ? ld_relaxed_s32(app.color + v) : 0;
+    const int32_t c = is_check ? ld_relaxed_s32(app.color + vg) : 0;
     bool self = false;
     int64_t e = is_check ? e0 : 0, ee = is_check ? e1 : 0;
     if (is_check) edges += ee - e;
@@ -303,15 +320,15 @@ __device__ __forceinline__ uint32_t gc_thread_task(const GcApp& app, const Graph
       if (e < ee) {
         u = (uint32_t)ld_stream_s32(g.col + e);
         ++e;
-        if (u != v && ld_relaxed_s32(app.color + u) == c) {
-          if (u < v) self = true;
-          else if (MODE == GC_UBER) {
+        if (u != vg && ld_relaxed_s32(app.color + u) == c) {
+          if (u < vg) self = true;
+          else if (MODE == GC_UBER && app.owned(u)) {
             __threadfence();
-            act = atomicExch(app.pend + u, 1u) == 0u;
+            act = atomicExch(app.pend + (u - app.vb), 1u) == 0u;
           }
         }
       }
-      if (MODE == GC_UBER) pushed += sink.warp_push(act, u);
+      if (MODE == GC_UBER) pushed += sink.warp_push(act, u - app.vb);
     }
     bool act = false;
     if (self) {
@@ -337,7 +354,7 @@ __device__ __forceinline__ uint32_t gc_thread_task(const GcApp& app, const Graph
       edges += ee - e;
       for (; e < ee; ++e) {
         const uint32_t u = (uint32_t)ld_stream_s32(g.col + e);
-        if (u == v) continue;
+        if (u == vg) continue;
         const int32_t r = ld_relaxed_s32(app.color + u) - base;
         if (r >= 0 && r < 64) m |= 1ull << r;
       }
@@ -348,7 +365,8 @@ __device__ __forceinline__ uint32_t gc_thread_task(const GcApp& app, const Graph
     }
     bool act = false;
     if (is_assign) {
-      st_relaxed_s32(app.color + v, chosen);
+      st_relaxed_s32(app.color + vg, chosen);
+      app.assigned(v);
       __threadfence();
       act = (MODE == GC_UBER);
     }

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import CStats, Config, _check, _cfg, lib
 
-APP_BFS, APP_PR = 0, 1
+APP_BFS, APP_PR, APP_GC = 0, 1, 2
 
 
 def block_bounds(n: int, world: int) -> np.ndarray:
@@ -35,7 +35,8 @@ def local_csr(off: np.ndarray, col: np.ndarray, vb: int, ve: int):
 class PartGraph:
     """This rank's partition (atos_graph_create_partitioned)."""
 
-    def __init__(self, global_n: int, world: int, rank: int, bounds, local_off, local_col, validate=False):
+    def __init__(self, global_n: int, world: int, rank: int, bounds, local_off, local_col, validate=False,
+                 symmetric=False):
         L = lib()
         self.global_n, self.world, self.rank = int(global_n), int(world), int(rank)
         self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
@@ -45,7 +46,7 @@ class PartGraph:
         h = ctypes.c_void_p()
         _check(L.atos_graph_create_partitioned(self.global_n, self.world, self.rank, self.bounds.ctypes.data,
                                                lo.ctypes.data, lc.ctypes.data if lc.size else None, lc.shape[0],
-                                               4 if validate else 0, ctypes.byref(h)),
+                                               (4 if validate else 0) | (8 if symmetric else 0), ctypes.byref(h)),
                "atos_graph_create_partitioned")
         self.h = h
 
@@ -53,6 +54,7 @@ class PartGraph:
     def from_global(cls, g, world: int, rank: int, bounds=None, **kw):
         b = block_bounds(g.n, world) if bounds is None else np.asarray(bounds, dtype=np.int64)
         lo, lc = local_csr(g.off, g.col, int(b[rank]), int(b[rank + 1]))
+        kw.setdefault("symmetric", bool(getattr(g, "symmetric", False)))
         return cls(g.n, world, rank, b, lo, lc, **kw)
 
     def close(self):
@@ -73,7 +75,7 @@ def _ptr(t):
 
 def run(pg: PartGraph, app: int, src: int = 0, alpha: float = 0.85, eps: float = 1e-6,
         cfg: Config | None = None, group=None, **kw):
-    """Run a partitioned BFS (app 0) or PageRank (app 1) on this rank.
+    """Run a partitioned BFS (app 0), PageRank (app 1) or colouring (app 2) on this rank.
 
     Returns (local result numpy array, stats dict).  Collective: every rank of
     ``group`` must call it with the same arguments."""
@@ -101,7 +103,7 @@ def run(pg: PartGraph, app: int, src: int = 0, alpha: float = 0.85, eps: float =
         total = torch.tensor([int(counts_all.sum())], dtype=torch.int64, device=dev)
         dist.all_reduce(total, group=group)
         if int(total.item()) == 0:
-            if app == APP_BFS or flush_all:
+            if app != APP_PR or flush_all:
                 break
             flush_all = 1  # PageRank: close with a round that sends every pending contribution
             continue
@@ -117,7 +119,7 @@ def run(pg: PartGraph, app: int, src: int = 0, alpha: float = 0.85, eps: float =
         if not host:
             torch.cuda.current_stream().synchronize()
         _check(L.atos_part_apply(pg.h, _ptr(recv), sum(rc)), "atos_part_apply")
-    out = np.empty(pg.n, dtype=np.uint32 if app == APP_BFS else np.float32)
+    out = np.empty(pg.n, dtype={APP_BFS: np.uint32, APP_PR: np.float32, APP_GC: np.int32}[app])
     st = CStats()
     _check(L.atos_part_finish(pg.h, out.ctypes.data if pg.n else None, ctypes.byref(st)), "atos_part_finish")
     return out, st.to_dict()
@@ -129,3 +131,22 @@ def bfs(pg: PartGraph, src: int, cfg: Config | None = None, group=None, **kw):
 
 def pagerank(pg: PartGraph, alpha: float = 0.85, eps: float = 1e-6, cfg: Config | None = None, group=None, **kw):
     return run(pg, APP_PR, alpha=alpha, eps=eps, cfg=cfg, group=group, **kw)
+
+
+def color(pg: PartGraph, cfg: Config | None = None, group=None, **kw):
+    """Partitioned speculative greedy colouring of a symmetric
+    graph.  Returns (local colours int32[n_local], stats) — stats["num_colors"] is
+    the colour count over all ranks (a MAX all-reduce)."""
+    import torch
+    import torch.distributed as dist
+
+    out, st = run(pg, APP_GC, cfg=cfg, group=group, **kw)
+    k = int(out.max()) + 1 if out.size else 0
+    if pg.world > 1:
+        host = dist.get_backend(group) == "gloo"
+        t = torch.tensor([k], dtype=torch.int64,
+                         device="cpu" if host else torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        k = int(t.item())
+    st["num_colors"] = k
+    return out, st

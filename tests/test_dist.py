@@ -65,6 +65,35 @@ def test_orchestration_gloo_fake_engine(world, tmp_path):
     assert int(parts[0]["rounds"]) == 0  # fake engine reports no stats
 
 
+def _check_partitioned_coloring(colors, parts):
+    g, fwd = gg.permute(gg.rmat(12, 8, seed=3, symmetrize=True), 7)
+    bad, k = oracle.check_coloring(g, colors)
+    assert bad == 0  # proper: zero monochromatic edges (exhaustive scan)
+    assert np.all(colors >= 0) and np.all(colors <= g.degrees())  # first fit: colour <= degree
+    assert all(int(p["num_colors"]) == k for p in parts)  # every rank reports the global count
+    return g, k
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_coloring_protocol_gloo_fake_engine(world, tmp_path):
+    """The cross-rank colouring protocol (ghost replica, changed-colour
+    messages, larger endpoint recolours) with real gloo collectives and a serial
+    numpy stand-in for each rank's kernel: the union is a proper colouring."""
+    colors, parts = _spawn(world, "fake", 2, tmp_path)
+    g, k = _check_partitioned_coloring(colors, parts)
+    assert k <= int(g.degrees().max()) + 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,mode,worker", [(2, "gpu", "cta"), (3, "gpu", "cta"), (3, "gpu", "warp"),
+                                               (2, "gpu", "thread"), (2, "gpu-discrete", "warp")])
+def test_gpu_partitioned_coloring_multiprocess(world, mode, worker, tmp_path, monkeypatch):
+    monkeypatch.setenv("ATOS_TEST_WORKER", worker)
+    colors, parts = _spawn(world, mode, 2, tmp_path)
+    _check_partitioned_coloring(colors, parts)
+    assert sum(int(p["bytes"]) for p in parts) > 0  # ghost colours were exchanged
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,mode", [(2, "gpu"), (3, "gpu"), (3, "gpu-discrete")])
 def test_gpu_partitioned_bfs_multiprocess(world, mode, tmp_path):
@@ -98,3 +127,12 @@ def test_gpu_partitioned_world1():
         adist.PartGraph(g.n, 2, 0, [0, 5, 3], g.off[:6], g.col[:g.off[5]])
     with pytest.raises(atos.AtosError):  # a partitioned handle is not a single-GPU graph
         atos.bfs(pg, 0)
+    with pytest.raises(atos.AtosError) as e:  # colouring needs a symmetric graph
+        adist.color(pg)
+    assert e.value.name == "INVALID_GRAPH"
+    s = gg.rmat(13, 16, seed=2, symmetrize=True)
+    ps = adist.PartGraph.from_global(s, 1, 0)
+    for w in ("cta", "warp", "thread"):
+        c, st = adist.color(ps, worker=w)
+        bad, k = oracle.check_coloring(s, c)
+        assert bad == 0 and st["num_colors"] == k
