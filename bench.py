@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--pr-threads", type=int, default=512, help="PageRank cta_threads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-color", action="store_true", help="skip the time-to-colour leg (symmetrised graph)")
     ap.add_argument("--dist-kernel-bfs", default="persistent", choices=["persistent", "discrete"],
                     help="N > 1, BFS: per-round local strategy (persistent = drain to local quiescence)")
     ap.add_argument("--dist-kernel-pr", default="discrete", choices=["persistent", "discrete"],
@@ -178,7 +179,7 @@ def run_reference(args, rank, world):
     }), flush=True)
 
 
-def cpu_baseline(g, depth_gpu):
+def cpu_baseline(g, depth_gpu, gs=None, colors_gpu=None):
     import oracle
     deg = g.degrees()
     jac_iters = 2
@@ -188,10 +189,18 @@ def cpu_baseline(g, depth_gpu):
     oracle.pagerank(g, ALPHA, tol=0.0, max_iter=jac_iters, threads=1)
     t2 = time.perf_counter()
     e = int(deg[d != oracle.UNREACHED].sum()) + jac_iters * g.m
-    return {"value": e / (t2 - t0) / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
-            "sample": f"serial FIFO BFS from 0 on the full graph ({t1 - t0:.1f} s) + {jac_iters} fp64 Jacobi "
-                      f"sweeps, 1 thread ({t2 - t1:.1f} s)",
-            "bfs_matches_gpu": bool(np.array_equal(d, depth_gpu))}
+    out = {"value": e / (t2 - t0) / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+           "sample": f"serial FIFO BFS from 0 on the full graph ({t1 - t0:.1f} s) + {jac_iters} fp64 Jacobi "
+                     f"sweeps, 1 thread ({t2 - t1:.1f} s)",
+           "bfs_matches_gpu": bool(np.array_equal(d, depth_gpu))}
+    if gs is not None:
+        t3 = time.perf_counter()
+        _, k = oracle.greedy_color(gs)
+        t4 = time.perf_counter()
+        bad, kg = oracle.check_coloring(gs, colors_gpu)
+        out["color"] = {"time_to_color_ms": (t4 - t3) * 1e3, "colors": k, "kind": "serial id-order first fit",
+                        "gpu_monochromatic_edges": bad, "gpu_colors": kg}
+    return out
 
 
 # ------------------------------------------------------------------ atos
@@ -298,10 +307,39 @@ def run_atos(args, rank, world, local_rank):
     }
     if not args.no_e2e:
         out["e2e"] = e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world)
+    gs = colors = None
+    if not args.no_color:
+        gs, colors, out["color"] = color_leg(args, atos, dev, flush)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline(g, d_host)
+        out["cpu_baseline"] = cpu_baseline(g, d_host, gs, colors)
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def color_leg(args, atos, dev, flush):
+    """Time-to-colour (the metric's third part): speculative greedy colouring
+    (Alg. 6, persistent CTA workers) of the symmetrised RMAT graph, device time
+    of the library call (init + run) with L2 flushed before each run."""
+    import torch
+    import graphgen as gg
+    t = time.time()
+    gs = gg.rmat(args.scale, args.edge_factor, seed=1, symmetrize=True)
+    gen_s = time.time() - t
+    S = atos.Graph(gs.off, gs.col, symmetric=True)
+    cfg = atos.Config(kernel="persistent", worker="cta", fetch_size=128, cta_threads=256, timeout_s=120)
+    out = torch.empty(gs.n, dtype=torch.int32, device=dev)
+    atos.color(S, cfg, out=out)  # warm-up
+    ms, k = [], 0
+    for _ in range(3):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        _, k, st = atos.color(S, cfg, out=out)
+        ms.append(st["ms"])
+    S.close()
+    return gs, out.cpu().numpy(), {
+        "time_to_color_ms": statistics.median(ms), "ms_all": ms, "colors": k, "overwork": st["tasks_popped"] / (2 * gs.n),
+        "graph": f"rmat{args.scale}_ef{args.edge_factor} symmetrised (n={gs.n}, m={gs.m})", "graph_gen_s": gen_s,
+        "kernel": "persistent", "worker": "cta", "fetch_size": 128, "cta_threads": 256}
 
 
 def e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world):
@@ -421,8 +459,41 @@ def run_atos_multi(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     out["roofline"]["frac"] = out["roofline"]["achieved"] / hbm
+    if not args.no_color:
+        out["color"] = color_leg_multi(args, rank, world, dev, flush)
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def color_leg_multi(args, rank, world, dev, flush):
+    """Time-to-colour on N GPUs: partitioned speculative colouring of
+    the symmetrised, permuted RMAT graph; device time = CUDA events around the
+    whole multi-round call (exchanges included), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import graphgen as gg
+    from paper_2112_00132_b200 import dist as adist
+    gs, _ = gg.permute(gg.rmat(args.scale, args.edge_factor, seed=1, symmetrize=True), 12345)
+    pg = adist.PartGraph.from_global(gs, world, rank)
+    stream = torch.cuda.current_stream()
+    ms, k, st = [], 0, {}
+    for i in range(4):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c, st = adist.color(pg, timeout_s=300)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            ms.append(e0.elapsed_time(e1))
+    t = torch.tensor(ms, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    pg.close()
+    return {"time_to_color_ms": float(t.median().item()), "colors": st["num_colors"], "rounds": st["rounds"],
+            "graph": f"rmat{args.scale}_ef{args.edge_factor} symmetrised + permuted (n={gs.n}, m={gs.m})",
+            "parallelism": f"1d-partition x{world}", "kernel": "persistent", "worker": "cta"}
 
 
 def main():
