@@ -80,7 +80,10 @@ typedef struct {
   int32_t stage_edges;    /* persistent CTA workers: column-list staging per batch buffer via   */
                           /*   TMA bulk copies, in edges; 0 = off (default), -1 =   */
                           /*   auto (largest that keeps occupancy and 64 KB of L1 per SM)       */
-  int32_t _pad0;
+  int32_t sink_defer;     /* 1 (default): never push a dangling (out-degree 0) vertex (R29).     */
+                          /*   BFS: its depth is already final in dist[] (its task expands no   */
+                          /*   edge).  PageRank (threshold activation): its task is rank += exch */
+                          /*   (res) with no other effect, applied once after quiescence.       */
 } atos_config;
 
 /* One timeline record per batch processed by a persistent/discrete worker:

@@ -55,7 +55,7 @@ class CConfig(ctypes.Structure):
                 ("adaptive_fetch", ctypes.c_int32), ("device_loop", ctypes.c_int32),
                 ("queue_capacity", ctypes.c_int64), ("timeout_s", ctypes.c_double),
                 ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64),
-                ("stage_edges", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
+                ("stage_edges", ctypes.c_int32), ("sink_defer", ctypes.c_int32)]
 
 
 class CStats(ctypes.Structure):
@@ -138,6 +138,7 @@ class Config:
     stream: int | None = None      # raw cudaStream_t; None = torch current stream
     trace: object = None           # Trace() buffer for the timeline, or None
     stage_edges: int = 0           # TMA column staging per batch buffer (edges); 0 off, -1 auto
+    sink_defer: bool = True        # never push dangling vertices (BFS: no-op tasks; PR: one final pass) (R29)
 
     def to_c(self) -> CConfig:
         c = CConfig()
@@ -157,6 +158,7 @@ class Config:
         c.queue_capacity = self.queue_capacity
         c.timeout_s = self.timeout_s
         c.stage_edges = self.stage_edges
+        c.sink_defer = int(self.sink_defer)
         s = self.stream
         if s is None:
             import torch

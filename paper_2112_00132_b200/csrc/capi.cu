@@ -85,6 +85,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->timeout_s = 0.0;
   c->stream = nullptr;
   c->stage_edges = 0;  // off: measured slower on RMAT-24 (the staging smem costs L1 the probes use)
+  c->sink_defer = 1;
 }
 
 static atos_status check_config(const atos_config* c) {
@@ -197,6 +198,10 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
   unsigned long long hmd = 0;
   CK(cudaMemcpy(&hmd, md, sizeof hmd, cudaMemcpyDeviceToHost));
   g->max_degree = (int64_t)hmd;
+  // dangling-vertex bitmap (R29): a property of the immutable CSR, like the max degree
+  CK(cudaMalloc(&g->d_sink, (size_t)std::max<int64_t>(1, (n + 31) / 32) * sizeof(uint32_t)));
+  if (n) k_sink_bitmap<<<grid_for(n, 256, g->sms), 256>>>(g->d_off, n, g->d_sink);
+  CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return ATOS_OK;
 }
@@ -208,6 +213,7 @@ static void graph_free(atos_graph g) {
     cudaFree(g->d_col);
   }
   cudaFree(g->d_scratch);
+  cudaFree(g->d_sink);
   Workspace& w = g->ws;
   cudaFree(w.ring);
   cudaFree(w.ctl);
@@ -711,7 +717,7 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
   CK(cudaGetLastError());
   c.launches += 2;
   CK(cudaEventRecord(w.ev[1], c.s));
-  BfsApp app{w.u32a, w.u32b, w.u16a, c.cfg.bfs_filter};
+  BfsApp app{w.u32a, w.u32b, w.u16a, c.cfg.bfs_filter, c.cfg.sink_defer ? g->d_sink : nullptr};
   using P = EdgeMapPolicy<BfsApp>;
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
     CKS(run_persistent<P>(c, app, make_queue(g, c.cfg, 0)));
@@ -756,10 +762,13 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
                                                                        256, nullptr)));
   }
   if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
+  // R29: sink deferral for the threshold-activated queue strategies
+  const bool sinks = c.cfg.sink_defer && !bsp && c.cfg.pr_activation == 0;
+  const uint32_t* sink_bits = sinks ? g->d_sink : nullptr;
   CK(cudaGetLastError());
   c.launches += bsp ? 4 : 5;
   CK(cudaEventRecord(w.ev[1], c.s));
-  PrAppT<R> app{rank, res, (R)alpha, (R)eps};
+  PrAppT<R> app{rank, res, (R)alpha, (R)eps, sink_bits};
   if (c.cfg.pr_activation == 1) {
     if constexpr (std::is_same<R, float>::value) {
       // f1: Alg. 4's Check_Size window activation; every vertex starts queued
@@ -769,10 +778,16 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
       return ATOS_OK;
     }
   }
-  if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
-    CKS(run_persistent<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1)));
-  } else if (c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
-    CKS(run_discrete<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1), (uint64_t)n));
+  if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT || c.cfg.kernel == ATOS_KERNEL_DISCRETE) {
+    if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT)
+      CKS(run_persistent<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1)));
+    else
+      CKS(run_discrete<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1), (uint64_t)n));
+    if (sinks) {
+      k_pr_absorb_sinks<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(sink_bits, res, rank, n);
+      CK(cudaGetLastError());
+      c.launches++;
+    }
   } else {
     // Alg. 3: push kernel over the frontier, then filter kernel over all vertices
     PrBspAppT<R> bapp{app};

@@ -45,6 +45,7 @@ struct atos_graph_s {
   int64_t* d_off = nullptr;
   int32_t* d_col = nullptr;
   int64_t col_cap = 0;  // readable elements of d_col
+  uint32_t* d_sink = nullptr;  // bit v = (deg(v) == 0), built at create (R29)
   void* d_scratch = nullptr;
   bool owned = false;
   bool symmetric = false;

@@ -206,6 +206,11 @@ __device__ __forceinline__ int64_t ld_nc_s64(const int64_t* p) {  // CSR offsets
   asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol_evict_first()));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {  // immutable per-vertex bitmaps: keep in L2
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_last()));
+  return v;
+}
 __device__ __forceinline__ void st_stream_u64(uint64_t* p, uint64_t v) {  // queue slot writes
   asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol_evict_first()) : "memory");
 }

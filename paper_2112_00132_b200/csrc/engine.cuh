@@ -44,6 +44,9 @@ struct BfsApp {
   // missed 38% of probes into random DRAM sectors (profiles/r01_bfs_*).
   uint16_t* near;
   int filter;
+  // R29: bit w set = deg(w) == 0.  A dangling vertex's task expands no edge,
+  // so an improvement of dist[w] is final without pushing w.  nullptr = off.
+  const uint32_t* sink;
   using Payload = uint32_t;
   using Probe = uint32_t;
   // Chunk task of v created with payload nd: still current iff dist[v]+1 == nd.
@@ -69,8 +72,9 @@ struct BfsApp {
   }
   __device__ __forceinline__ bool decide(Payload nd, uint32_t w, Probe pr, Raw old) const {
     const bool improved = nd < pr && nd < old;
-    if (improved) st_u16_hot(near + w, nd < 0xFFFFu ? (uint16_t)nd : (uint16_t)0xFFFFu);
-    return improved;
+    if (!improved) return false;
+    st_u16_hot(near + w, nd < 0xFFFFu ? (uint16_t)nd : (uint16_t)0xFFFFu);
+    return sink == nullptr || !((ld_nc_u32(sink + (w >> 5)) >> (w & 31)) & 1u);
   }
   // Expand v at its CURRENT depth d (R3) unless some task already expanded
   // (or is expanding) v at depth <= d: a vertex pushed k times by k
@@ -127,7 +131,16 @@ struct PrAppT {
   double* rank;
   R* res;
   R alpha, eps;
+  // Sink deferral (R29): bit w set = deg(w) == 0.  A dangling vertex's task is
+  // `rank += exch(res)` with no effect on any other vertex, so its activation
+  // push is skipped and k_pr_absorb_sinks applies it once after quiescence.
+  // nullptr = off (every crossing is pushed, Alg. 4 literally).
+  const uint32_t* sink;
   using Payload = R;
+  __device__ __forceinline__ bool activates(R old, R c, uint32_t w) const {
+    if (!(old <= eps && add_rn(old, c) > eps)) return false;
+    return sink == nullptr || !((ld_nc_u32(sink + (w >> 5)) >> (w & 31)) & 1u);
+  }
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
     Pre x = begin_load(v, g);
@@ -154,19 +167,14 @@ struct PrAppT {
     p = alpha * x.r / (R)(x.e1 - x.e0);
     return true;
   }
-  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
-    const R old = atom_add_hot(res + w, c);
-    return old <= eps && add_rn(old, c) > eps;
-  }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const { return activates(atom_add_hot(res + w, c), c, w); }
   using Probe = int;
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
   __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
   using Raw = R;
   __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { return atom_add_hot(res + w, c); }
-  __device__ __forceinline__ bool decide(Payload c, uint32_t, Probe, Raw old) const {
-    return old <= eps && add_rn(old, c) > eps;
-  }
+  __device__ __forceinline__ bool decide(Payload c, uint32_t w, Probe, Raw old) const { return activates(old, c, w); }
 };
 
 // Asynchronous PageRank with the paper's own activation rule (Alg. 4 lines

@@ -401,6 +401,30 @@ __global__ void k_f64_to_f32(const double* a, float* b, int64_t n) {
     b[i] = (float)a[i];
 }
 
+// Sink bitmap for PageRank sink deferral (R29): bit v of word v/32 = (deg(v) == 0).
+__global__ void k_sink_bitmap(const int64_t* off, int64_t n, uint32_t* bits) {
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = b + lane_id();
+    const uint32_t m = __ballot_sync(FULL_MASK, v < n && off[v + 1] == off[v]);
+    if (lane_id() == 0) bits[b >> 5] = m;
+  }
+}
+
+// Sink absorption (R29): after quiescence every dangling vertex performs its
+// deferred task body `rank[v] += exch(res[v], 0)` (Alg. 4 line 8 with deg 0, R5).
+template <class R>
+__global__ void k_pr_absorb_sinks(const uint32_t* __restrict__ bits, R* res, double* rank, int64_t n) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if ((bits[v >> 5] >> (v & 31)) & 1u) {
+      const R r = res[v];
+      if (r != R(0)) {
+        rank[v] += (double)r;
+        res[v] = R(0);
+      }
+    }
+  }
+}
+
 // BSP PageRank filter kernel (Alg. 3 lines 18-22): residue > eps -> frontier
 template <class R>
 __global__ void k_pr_filter(const R* res, int64_t n, R eps, uint32_t* out, unsigned long long* count) {

@@ -75,6 +75,14 @@ def D(atos, name, symmetric=False):
 
 # ------------------------------------------------------------------ BFS ---
 
+def expandable(g, depth, src):
+    """Vertices a BFS must pop with sink deferral (R29): the reached vertices
+    with out-degree > 0, plus the source (always enqueued)."""
+    deg = np.diff(g.off)
+    reach = depth != oracle.UNREACHED
+    return int(np.sum(reach & (deg > 0))) + int(deg[src] == 0)
+
+
 @pytest.mark.parametrize("kernel,worker,fetch", list(itertools.product(KERNELS, WORKERS, FETCH)))
 @pytest.mark.parametrize("gname", ["grid64", "rmat16"])
 def test_bfs_matrix(atos, gname, kernel, worker, fetch):
@@ -83,8 +91,7 @@ def test_bfs_matrix(atos, gname, kernel, worker, fetch):
                      cta_threads=T(worker, fetch))
     exp = oracle.bfs(g, 0)
     assert np.array_equal(d, exp), f"{int(np.sum(d != exp))} mismatches"
-    reach = int(np.sum(exp != oracle.UNREACHED))
-    assert st["tasks_popped"] >= reach  # overwork >= 1
+    assert st["tasks_popped"] >= expandable(g, exp, 0)  # overwork >= 1
 
 
 def test_bfs_grid_manhattan(atos):
@@ -114,13 +121,38 @@ def test_bfs_special_graphs(atos, gname, src, worker):
 
 def test_bfs_serial_order_identity(atos):
     """One warp worker, FETCH 1, one CTA: FIFO order => Dijkstra order =>
-    every reachable vertex is popped exactly once (overwork 1.0)."""
+    every reachable vertex is popped exactly once (overwork 1.0, S:557);
+    with sink deferral (R29) every reachable non-dangling vertex."""
     for name in ["grid64", "rmat12", "road"]:
         g = G(name)
-        d, st = atos.bfs(D(atos, name), 0, worker="warp", fetch_size=1, num_blocks=1, cta_threads=32)
         exp = oracle.bfs(g, 0)
-        assert np.array_equal(d, exp)
-        assert st["tasks_popped"] == int(np.sum(exp != oracle.UNREACHED)), name
+        for defer in (False, True):
+            d, st = atos.bfs(D(atos, name), 0, worker="warp", fetch_size=1, num_blocks=1, cta_threads=32,
+                             sink_defer=defer)
+            assert np.array_equal(d, exp)
+            want = expandable(g, exp, 0) if defer else int(np.sum(exp != oracle.UNREACHED))
+            assert st["tasks_popped"] == want, (name, defer)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("worker", WORKERS)
+def test_bfs_sink_defer(atos, kernel, worker):
+    """R29: dangling vertices get their depth from the atomicMin and are never
+    pushed; depths stay bit-exact, pops drop to the expandable vertices."""
+    g = G("rmat16")
+    exp = oracle.bfs(g, 0)
+    pops = {}
+    for defer in (False, True):
+        d, st = atos.bfs(D(atos, "rmat16"), 0, kernel=kernel, worker=worker, fetch_size=32,
+                         cta_threads=T(worker, 32), sink_defer=defer)
+        assert np.array_equal(d, exp), (defer, int(np.sum(d != exp)))
+        pops[defer] = st["tasks_popped"]
+    assert pops[True] >= expandable(g, exp, 0)
+    assert pops[True] < pops[False], pops
+    # a dangling source is still popped once; its neighbours-less task ends the run
+    h = gg.from_edges(4, [(1, 0), (2, 0)])
+    d, st = atos.bfs(atos.Graph.from_csr(h), 0, kernel=kernel, worker=worker)
+    assert list(d) == [0, oracle.UNREACHED, oracle.UNREACHED, oracle.UNREACHED] and st["tasks_popped"] == 1
 
 
 def test_bfs_deep_path_beyond_u16_mirror(atos):
@@ -310,6 +342,38 @@ def test_pagerank_fp64_residue(atos, worker):
                               pr_residue_fp64=True)
         assert np.max(np.abs(r - x)) / x.max() <= PR_TOL
         assert st["max_residue"] <= 1e-6
+
+
+@pytest.mark.parametrize("kernel", ["persistent", "discrete"])
+@pytest.mark.parametrize("worker", WORKERS)
+def test_pagerank_sink_defer(atos, kernel, worker):
+    """R29: dangling vertices are never pushed on activation; their residue is
+    absorbed after quiescence.  Same fixed point (Jacobi), fewer
+    pushed tasks than the literal Alg. 4 activation (rmat16: 38% dangling)."""
+    x = jacobi("rmat16")
+    g = G("rmat16")
+    dangling = np.diff(g.off) == 0
+    assert dangling.mean() > 0.2
+    pushed = {}
+    for defer in (False, True):
+        r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
+                              cta_threads=T(worker, 32), pr_residue_fp64=worker == "thread", sink_defer=defer)
+        assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
+        assert st["max_residue"] <= 1e-6
+        assert np.all(r <= x * (1 + 1e-5) + 1e-6)
+        pushed[defer] = st["tasks_pushed"]
+    assert pushed[True] < pushed[False], pushed
+
+
+def test_pagerank_sink_defer_edge_cases(atos):
+    a = 0.85
+    # every vertex dangling: nothing propagates, rank = 1 - a
+    r, st = atos.pagerank(atos.Graph.from_csr(gg.empty(37)), a, 1e-6)
+    assert np.allclose(r, 1 - a) and st["tasks_pushed"] == 0
+    # directed chain 0->...->k: only the last vertex is dangling; x_i = 1 - a^(i+1)
+    for defer in (False, True):
+        r, _ = atos.pagerank(atos.Graph.from_csr(gg.directed_chain(6)), a, 1e-7, sink_defer=defer)
+        assert np.allclose(r, 1 - a ** (np.arange(6) + 1), atol=1e-5)
 
 
 @pytest.mark.parametrize("check_size", [1, 8, 32])
