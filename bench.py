@@ -280,7 +280,7 @@ def run_atos(args, rank, world, local_rank):
         "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_bfs0+pagerank", "scale": args.scale,
                    "edge_factor": args.edge_factor, "n": g.n, "m": g.m, "kernel": "persistent", "worker": "cta",
                    "fetch_size": args.fetch, "pr_fetch_size": args.pr_fetch, "cta_threads": args.threads,
-                   "pr_cta_threads": args.pr_threads,
+                   "pr_cta_threads": args.pr_threads, "sink_defer": True,
                    "alpha": ALPHA, "eps": EPS, "l2": "flushed (512 MB write) between steps; inputs 1.2 GB > L2",
                    "parallelism": "replicas" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": pr_ach, "peak": hbm, "unit": "GB/s", "frac": pr_ach / hbm,

@@ -752,21 +752,26 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
   CK(cudaEventRecord(w.ev[0], c.s));
   // a2: rank = 1 - alpha ; residue seeded by one synchronous push (R4) ; all vertices enqueued
   k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rank, n, 1.0 - (double)alpha);
-  k_fill<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, R(0));
+  // R30: the seeding sums accumulate in fp64 (w.f64b; the residue array itself when R = double)
+  // and are rounded once to R: fp32 adds of one repeated c = (1-a)a/deg(v) onto a hub's growing sum
+  // round with correlated errors (measured: RMAT-27's hub 4.8e-4 of max x* low, a fan-in test graph 1.7e-4)
+  double* acc = w.f64b;
+  k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, n, 0.0);
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
   {
-    PrInitAppT<R> ia{res, (R)(1.0 - (double)alpha) * (R)alpha};
+    PrInitAppT<double> ia{acc, (1.0 - (double)alpha) * (double)alpha};
     LaunchCtx ci = c;
     ci.cfg.worker = ATOS_WORKER_CTA;
-    CKS((bsp_step_w<EdgeMapPolicy<PrInitAppT<R>>, PrInitAppT<R>, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr, nullptr,
-                                                                       256, nullptr)));
+    CKS((bsp_step_w<EdgeMapPolicy<PrInitAppT<double>>, PrInitAppT<double>, W_CTA>(ci, ia, nullptr, (uint64_t)n,
+                                                                                 nullptr, nullptr, 256, nullptr)));
   }
+  if (!std::is_same<R, double>::value) k_f64_to_res<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, res, n);
   if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
   // R29: sink deferral for the threshold-activated queue strategies
   const bool sinks = c.cfg.sink_defer && !bsp && c.cfg.pr_activation == 0;
   const uint32_t* sink_bits = sinks ? g->d_sink : nullptr;
   CK(cudaGetLastError());
-  c.launches += bsp ? 4 : 5;
+  c.launches += (bsp ? 4 : 5) + (std::is_same<R, double>::value ? 0 : 1);
   CK(cudaEventRecord(w.ev[1], c.s));
   PrAppT<R> app{rank, res, (R)alpha, (R)eps, sink_bits};
   if (c.cfg.pr_activation == 1) {
@@ -833,8 +838,8 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   CKS(ensure(w.f32a, w.f32a_n, (size_t)n));
   CKS(ensure(w.f64a, w.f64a_n, (size_t)n));
   if (c.cfg.pr_activation == 1) CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // queued flags
-  if (r64) CKS(ensure(w.f64b, w.f64b_n, (size_t)n));
-  else CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
+  CKS(ensure(w.f64b, w.f64b_n, (size_t)n));  // fp64 residues, or the fp64 seeding accumulator (R30)
+  if (!r64) CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
   if (bsp) {
     CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
     CKS(ensure(w.front[1], w.front_n[1], (size_t)n));

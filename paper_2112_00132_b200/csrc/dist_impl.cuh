@@ -474,24 +474,25 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
   } else {
     CKS(ensure(w.f32a, w.f32a_n, (size_t)std::max<int64_t>(n, 1)));
     CKS(ensure(w.f64a, w.f64a_n, (size_t)std::max<int64_t>(n, 1)));
-    if (d->r64) CKS(ensure(w.f64b, w.f64b_n, (size_t)std::max<int64_t>(n, 1)));
-    else CKS(ensure(w.f32b, w.f32b_n, (size_t)std::max<int64_t>(n, 1)));
+    CKS(ensure(w.f64b, w.f64b_n, (size_t)std::max<int64_t>(n, 1)));  // residues or the fp64 seeding sums (R30)
+    if (!d->r64) CKS(ensure(w.f32b, w.f32b_n, (size_t)std::max<int64_t>(n, 1)));
     if (!d->racc) CK(cudaMalloc(&d->racc, (size_t)N * sizeof(float)));
     CK(cudaMemsetAsync(d->racc, 0, (size_t)N * sizeof(float), c.s));
     k_fill<double><<<fill_blocks(std::max<int64_t>(n, 1), g->sms), 256, 0, c.s>>>(w.f64a, n, 1.0 - (double)alpha);
     k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, (uint64_t)n, w.ring, -1);
     if (n) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
-    auto init = [&](auto* res) -> atos_status {
-      using R = std::remove_pointer_t<decltype(res)>;
-      k_fill<R><<<fill_blocks(std::max<int64_t>(n, 1), g->sms), 256, 0, c.s>>>(res, n, R(0));
-      PrPartInitAppT<R> ia{res, d->racc, (R)(1.0 - (double)alpha) * (R)alpha, (uint32_t)g->v_begin, (uint32_t)g->v_end};
+    // R30: local seeding sums accumulate in fp64 and are rounded once (remote ones go to racc)
+    if (n) {
+      k_fill<double><<<fill_blocks(std::max<int64_t>(n, 1), g->sms), 256, 0, c.s>>>(w.f64b, n, 0.0);
+      PrPartInitAppT<double> ia{w.f64b, d->racc, (1.0 - (double)alpha) * (double)alpha, (uint32_t)g->v_begin,
+                                (uint32_t)g->v_end};
       LaunchCtx ci = c;
       ci.cfg.worker = ATOS_WORKER_CTA;
-      return bsp_step_w<EdgeMapPolicy<PrPartInitAppT<R>>, PrPartInitAppT<R>, W_CTA>(ci, ia, nullptr, (uint64_t)n,
-                                                                                    nullptr, nullptr, 256, nullptr);
-    };
-    if (n) CKS(d->r64 ? init(w.f64b) : init(w.f32b));
-    d->launches += 5;
+      CKS((bsp_step_w<EdgeMapPolicy<PrPartInitAppT<double>>, PrPartInitAppT<double>, W_CTA>(
+          ci, ia, nullptr, (uint64_t)n, nullptr, nullptr, 256, nullptr)));
+      if (!d->r64) k_f64_to_res<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.f64b, w.f32b, n);
+    }
+    d->launches += d->r64 ? 5 : 6;
   }
   CK(cudaGetLastError());
   CK(cudaEventRecord(w.ev[1], c.s));

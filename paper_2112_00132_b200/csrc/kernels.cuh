@@ -396,6 +396,12 @@ struct PrInitAppT {
   __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
 };
 
+template <class R>
+__global__ void k_f64_to_res(const double* a, R* b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (R)a[i];
+}
+
 __global__ void k_f64_to_f32(const double* a, float* b, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (float)a[i];

@@ -376,6 +376,32 @@ def test_pagerank_sink_defer_edge_cases(atos):
         assert np.allclose(r, 1 - a ** (np.arange(6) + 1), atol=1e-5)
 
 
+def fan_in_graph(k=40000, fan=64):
+    """k sources s -> 0 and s -> s+1 (chain), plus 0 -> 1..fan: vertex 0's
+    seeding residue (R4) is k adds of the same c = (1-a)a/2 onto a sum growing
+    to ~2,550, whose fp32 rounding errors are correlated (R30)."""
+    edges = [(s, 0) for s in range(1, k + 1)] + [(s, s + 1) for s in range(1, k)] + [(0, j) for j in range(1, fan + 1)]
+    return gg.from_edges(k + 1, edges, name="fanin")
+
+
+@pytest.mark.parametrize("kernel", ["persistent", "discrete"])
+@pytest.mark.parametrize("worker", WORKERS)
+def test_pagerank_fp64_seeding(atos, kernel, worker):
+    """R30: the seeding sums are accumulated in fp64 and rounded once, so the
+    fp32-residue result meets the tolerance on a fan-in hub (fp32 seeding
+    adds measured 1.7e-4 of max x* here, and 4.8e-4 on RMAT-27's hub)."""
+    g = fan_in_graph()
+    x = oracle.pagerank(g, 0.85)[0]
+    # thread workers holding 32 claimed vertices per lane also need fp64 residues in the
+    # main phase (test_pagerank_matrix, R26); they run with fetch 1 here instead
+    f = 1 if worker == "thread" else 32
+    r, st = atos.pagerank(atos.Graph.from_csr(g), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=f,
+                          cta_threads=T(worker, f))
+    err = np.max(np.abs(r.astype(np.float64) - x)) / x.max()
+    assert err <= PR_TOL, err
+    assert st["max_residue"] <= 1e-6
+
+
 @pytest.mark.parametrize("check_size", [1, 8, 32])
 @pytest.mark.parametrize("gname", ["rmat16", "grid64", "star", "road", "hub", "two"])
 def test_pagerank_window_activation(atos, gname, check_size):
