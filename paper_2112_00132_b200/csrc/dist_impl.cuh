@@ -150,7 +150,7 @@ template <class R>
 struct PrPartInitAppT {
   static constexpr bool kWindow = false;
   R* res;
-  float* racc;
+  R* racc;
   R c0;
   uint32_t vb, ve;
   using Payload = R;
@@ -168,7 +168,7 @@ struct PrPartInitAppT {
   __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
   __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const {
     if (w >= vb && w < ve) atomicAdd(res + (w - vb), c);
-    else atomicAdd(racc + w, (float)c);
+    else atomicAdd(racc + w, c);
     return 0;
   }
   __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
@@ -321,6 +321,7 @@ struct DistState {
   unsigned long long* h_cnt = nullptr;  // pinned
   uint32_t* sent_min = nullptr;
   float* racc = nullptr;
+  double* racc64 = nullptr;     // seeding sums of remote targets (R30), rounded into racc
   int32_t* gc_color = nullptr;  // colouring: replica of all N colours
   uint8_t* gc_chg = nullptr;    // colouring: local vertex changed colour this round
   uint8_t* gc_gchg = nullptr;   // colouring: ghost changed this round (global ids)
@@ -343,6 +344,7 @@ void dist_free(atos_graph g) {
   if (d->h_cnt) cudaFreeHost(d->h_cnt);
   cudaFree(d->sent_min);
   cudaFree(d->racc);
+  cudaFree(d->racc64);
   cudaFree(d->gc_color);
   cudaFree(d->gc_chg);
   cudaFree(d->gc_gchg);
@@ -484,15 +486,18 @@ extern "C" atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, f
     // R30: local seeding sums accumulate in fp64 and are rounded once (remote ones go to racc)
     if (n) {
       k_fill<double><<<fill_blocks(std::max<int64_t>(n, 1), g->sms), 256, 0, c.s>>>(w.f64b, n, 0.0);
-      PrPartInitAppT<double> ia{w.f64b, d->racc, (1.0 - (double)alpha) * (double)alpha, (uint32_t)g->v_begin,
+      if (!d->racc64) CK(cudaMalloc(&d->racc64, (size_t)N * sizeof(double)));
+      k_fill<double><<<fill_blocks(N, g->sms), 256, 0, c.s>>>(d->racc64, N, 0.0);
+      PrPartInitAppT<double> ia{w.f64b, d->racc64, (1.0 - (double)alpha) * (double)alpha, (uint32_t)g->v_begin,
                                 (uint32_t)g->v_end};
       LaunchCtx ci = c;
       ci.cfg.worker = ATOS_WORKER_CTA;
       CKS((bsp_step_w<EdgeMapPolicy<PrPartInitAppT<double>>, PrPartInitAppT<double>, W_CTA>(
           ci, ia, nullptr, (uint64_t)n, nullptr, nullptr, 256, nullptr)));
       if (!d->r64) k_f64_to_res<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.f64b, w.f32b, n);
+      k_f64_to_res<float><<<fill_blocks(N, g->sms), 256, 0, c.s>>>(d->racc64, d->racc, N);
     }
-    d->launches += d->r64 ? 5 : 6;
+    d->launches += n ? (d->r64 ? 7 : 8) : 2;
   }
   CK(cudaGetLastError());
   CK(cudaEventRecord(w.ev[1], c.s));

@@ -1,4 +1,5 @@
 # round-1 final-ish measurement pass: phase profile, bench, launch list, ncu full captures
+timeout 300 python -m pytest tests -m gpu -x -q -k "fp64_seeding or sink" > gpurun_out/gpu_tests5.log 2>&1
 set -x
 for app in bfs pr; do
   thr=256; [ $app = pr ] && thr=512
