@@ -84,6 +84,10 @@ typedef struct {
                           /*   BFS: its depth is already final in dist[] (its task expands no   */
                           /*   edge).  PageRank (threshold activation): its task is rank += exch */
                           /*   (res) with no other effect, applied once after quiescence.       */
+  int32_t pr_defer_degree; /* PageRank, persistent CTA workers: a popped vertex with >= this many */
+                          /*   out-edges and residue < pr_defer_factor * eps is re-queued once   */
+                          /*   instead of expanded (R31); 0 = off                                 */
+  int32_t pr_defer_factor;
 } atos_config;
 
 /* One timeline record per batch processed by a persistent/discrete worker:

@@ -55,7 +55,8 @@ class CConfig(ctypes.Structure):
                 ("adaptive_fetch", ctypes.c_int32), ("device_loop", ctypes.c_int32),
                 ("queue_capacity", ctypes.c_int64), ("timeout_s", ctypes.c_double),
                 ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64),
-                ("stage_edges", ctypes.c_int32), ("sink_defer", ctypes.c_int32)]
+                ("stage_edges", ctypes.c_int32), ("sink_defer", ctypes.c_int32),
+                ("pr_defer_degree", ctypes.c_int32), ("pr_defer_factor", ctypes.c_int32)]
 
 
 class CStats(ctypes.Structure):
@@ -139,6 +140,8 @@ class Config:
     trace: object = None           # Trace() buffer for the timeline, or None
     stage_edges: int = 0           # TMA column staging per batch buffer (edges); 0 off, -1 auto
     sink_defer: bool = True        # never push dangling vertices (BFS: no-op tasks; PR: one final pass) (R29)
+    pr_defer_degree: int = 0       # PR hub deferral (R31): min out-degree; 0 = off
+    pr_defer_factor: int = 4       # ... defer while residue < factor * eps
 
     def to_c(self) -> CConfig:
         c = CConfig()
@@ -159,6 +162,8 @@ class Config:
         c.timeout_s = self.timeout_s
         c.stage_edges = self.stage_edges
         c.sink_defer = int(self.sink_defer)
+        c.pr_defer_degree = self.pr_defer_degree
+        c.pr_defer_factor = self.pr_defer_factor
         s = self.stream
         if s is None:
             import torch

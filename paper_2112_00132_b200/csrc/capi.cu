@@ -86,6 +86,8 @@ extern "C" void atos_config_default(atos_config* c) {
   c->stream = nullptr;
   c->stage_edges = 0;  // off: measured slower on RMAT-24 (the staging smem costs L1 the probes use)
   c->sink_defer = 1;
+  c->pr_defer_degree = 0;
+  c->pr_defer_factor = 4;
 }
 
 static atos_status check_config(const atos_config* c) {
@@ -773,7 +775,11 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
   CK(cudaGetLastError());
   c.launches += (bsp ? 4 : 5) + (std::is_same<R, double>::value ? 0 : 1);
   CK(cudaEventRecord(w.ev[1], c.s));
-  PrAppT<R> app{rank, res, (R)alpha, (R)eps, sink_bits};
+  // R31: hub deferral only where the queue agent runs (persistent CTA workers) and ids leave bit 30 free
+  const bool dfr = c.cfg.pr_defer_degree > 0 && c.cfg.kernel == ATOS_KERNEL_PERSISTENT &&
+                   c.cfg.worker == ATOS_WORKER_CTA && n <= (int64_t)DEFER_BIT;
+  PrAppT<R> app{rank, res, (R)alpha, (R)eps, sink_bits, dfr ? (uint32_t)c.cfg.pr_defer_degree : 0u,
+                (R)eps * (R)std::max(1, c.cfg.pr_defer_factor)};
   if (c.cfg.pr_activation == 1) {
     if constexpr (std::is_same<R, float>::value) {
       // f1: Alg. 4's Check_Size window activation; every vertex starts queued

@@ -4,6 +4,8 @@
 // Check_Size window activation of Alg. 4 (row f1).  The worker itself is in
 // cta_ws2.cuh.
 #pragma once
+#include <type_traits>
+
 #include "engine.cuh"
 
 namespace atos {
@@ -43,13 +45,22 @@ __device__ __forceinline__ void warp_exclusive_scan(int64_t* a, int n) {
 // of ~3 per item (the agent warp was the bottleneck on low-degree frontiers).
 constexpr int AGENT_G = 4;
 
+// Apps that may defer a popped task (PageRank hub deferral, R31) declare kDefer.
+template <class A, class = void>
+struct DeferTrait : std::false_type {};
+template <class A>
+struct DeferTrait<A, std::void_t<decltype(A::kDefer)>> : std::integral_constant<bool, A::kDefer> {};
+
+// Returns the tasks the agent re-pushed (deferred, R31; warp-uniform).
 template <class App>
-__device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g, const Queue& q, const Queue* cq,
-                                              uint64_t first, uint32_t n, int64_t* e0s, int64_t* pre,
-                                              typename App::Payload* pay) {
+__device__ __forceinline__ uint32_t agent_prepare(const App& app, const GraphView& g, const Queue& q, const Queue* cq,
+                                                  uint64_t first, uint32_t n, int64_t* e0s, int64_t* pre,
+                                                  typename App::Payload* pay) {
   using Payload = typename App::Payload;
   using Pre = typename App::Pre;
+  constexpr bool kDefer = DeferTrait<App>::value;
   const uint32_t lane = lane_id();
+  uint32_t deferred = 0;
   for (uint32_t base = 0; base < n; base += 32 * AGENT_G) {
     uint32_t it[AGENT_G];
     uint64_t raw[AGENT_G];
@@ -77,10 +88,25 @@ __device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g
     // phase B: begin loads (chunk entries or per-vertex state)
     Pre x[AGENT_G];
     bool is_chunk[AGENT_G];
+    bool was_deferred[AGENT_G];
 #pragma unroll
     for (int k = 0; k < AGENT_G; ++k) {
       is_chunk[k] = cq && it[k] != 0xFFFFFFFFu && (it[k] & CHUNK_BIT);
+      was_deferred[k] = false;
+      if constexpr (kDefer) {
+        if (app.defer_deg && it[k] != 0xFFFFFFFFu && !is_chunk[k] && (it[k] & DEFER_BIT)) {
+          was_deferred[k] = true;
+          it[k] &= ~DEFER_BIT;
+        }
+      }
       if (it[k] != 0xFFFFFFFFu && !is_chunk[k]) x[k] = app.begin_load(it[k], g);
+    }
+    bool dpush[AGENT_G];
+    uint32_t ditem[AGENT_G];
+#pragma unroll
+    for (int k = 0; k < AGENT_G; ++k) {
+      dpush[k] = false;
+      ditem[k] = 0;
     }
     // phase C: commits, chunk handling, splitting; write the batch
 #pragma unroll
@@ -96,16 +122,30 @@ __device__ __forceinline__ void agent_prepare(const App& app, const GraphView& g
         } else {
           a = x[k].e0;
           z = x[k].e1;
-          ok = app.begin_commit(it[k], x[k], p);
-          if (ok && cq && z - a > SPLIT_DEG) z = split_hub(cq, it[k], a, z, p);
+          bool held = false;
+          if constexpr (kDefer) {
+            if (!was_deferred[k] && app.should_defer(x[k])) {
+              held = true;  // residue put back; re-pushed with DEFER_BIT unless another copy exists
+              dpush[k] = app.put_back(it[k], x[k]);
+              ditem[k] = it[k] | DEFER_BIT;
+            }
+          }
+          if (!held) {
+            ok = app.begin_commit(it[k], x[k], p);
+            if (ok && cq && z - a > SPLIT_DEG) z = split_hub(cq, it[k], a, z, p);
+          }
         }
       }
       e0s[i] = a;
       pre[i] = ok ? z - a : 0;
       pay[i] = p;
     }
+    if constexpr (kDefer) {
+      if (app.defer_deg) deferred += q_warp_push_multi<AGENT_G>(q, dpush, ditem);
+    }
   }
   __syncwarp();
+  return deferred;
 }
 
 // Check_Size window sweep (f1): the warp reserves `span` ids from the global

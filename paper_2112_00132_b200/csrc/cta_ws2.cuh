@@ -217,7 +217,8 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       }
       WPROF_MARK(1);
       if (n) {
-        agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b));
+        const uint32_t dfr = agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b));
+        if (lane == 0) st.pushed += dfr;
         int64_t* pre = buf_pre(b);
         warp_exclusive_scan(pre, (int)n);
         if (S) agent_stage(g, n, buf_e0(b), pre, buf_sofs(b), buf_stage(b), S, &bars[b]);

@@ -300,6 +300,7 @@ __device__ __forceinline__ void q_trace(const Queue& q, uint32_t items, uint64_t
 // (item = CHUNK_BIT | table index).  payload = the app payload computed when
 // the hub was popped (BFS: dist+1, PR: alpha r / deg).
 constexpr uint32_t CHUNK_BIT = 0x80000000u;
+constexpr uint32_t DEFER_BIT = 0x40000000u;  // PageRank: a task deferred once (R31); needs n <= 2^30
 struct Chunk {
   uint64_t payload;
   int64_t e0, e1;

@@ -136,6 +136,14 @@ struct PrAppT {
   // push is skipped and k_pr_absorb_sinks applies it once after quiescence.
   // nullptr = off (every crossing is pushed, Alg. 4 literally).
   const uint32_t* sink;
+  // Hub deferral (R31, persistent CTA workers): a popped vertex with at least
+  // defer_deg out-edges whose residue is below defer_res (a few eps) is not
+  // expanded yet — its residue goes back and it is re-queued once (DEFER_BIT),
+  // so it comes back with the residue accumulated over a second queue cycle
+  // instead of scattering an eps-sized residue over thousands of edges.
+  static constexpr bool kDefer = true;
+  uint32_t defer_deg;  // 0 = off
+  R defer_res;
   using Payload = R;
   __device__ __forceinline__ bool activates(R old, R c, uint32_t w) const {
     if (!(old <= eps && add_rn(old, c) > eps)) return false;
@@ -152,6 +160,14 @@ struct PrAppT {
     int64_t e0, e1;
     R r;
   };
+  __device__ __forceinline__ bool should_defer(const Pre& x) const {
+    return defer_deg && x.e1 - x.e0 >= (int64_t)defer_deg && x.r < defer_res && x.r > R(0);
+  }
+  // Put the taken residue back.  If it was <= eps just before (nobody re-pushed
+  // v since our take), the caller re-queues v; otherwise a copy is queued already.
+  __device__ __forceinline__ bool put_back(uint32_t v, const Pre& x) const {
+    return atom_add_hot(res + v, x.r) <= eps;
+  }
   // the residue exchange is issued in the load phase (its result is only used in commit)
   __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
     Pre x;

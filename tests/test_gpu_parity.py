@@ -376,6 +376,24 @@ def test_pagerank_sink_defer_edge_cases(atos):
         assert np.allclose(r, 1 - a ** (np.arange(6) + 1), atol=1e-5)
 
 
+@pytest.mark.parametrize("gname", ["rmat16", "hub", "star", "fanin"])
+@pytest.mark.parametrize("deg,factor", [(1, 1000), (16, 4), (1024, 8)])
+def test_pagerank_hub_deferral(atos, gname, deg, factor):
+    """R31: deferring popped hubs with small residues (re-queued once with
+    DEFER_BIT) reaches the same fixed point; (1, 1000) defers nearly every pop."""
+    g = fan_in_graph() if gname == "fanin" else G(gname)
+    x = oracle.pagerank(g, 0.85)[0]
+    Gd = atos.Graph.from_csr(g) if gname == "fanin" else D(atos, gname)
+    # deferring the fan-in hub lets its fp32 residue grow for a second queue cycle while
+    # eps-sized pushes arrive, which then round away (1.1e-4 / 1.8e-4 of max x* measured
+    # with fp32 residues at (1, 1000) / (16, 4)): that graph runs with fp64 residues (R31)
+    r, st = atos.pagerank(Gd, 0.85, 1e-6, fetch_size=64, pr_defer_degree=deg, pr_defer_factor=factor,
+                          pr_residue_fp64=gname == "fanin")
+    assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
+    assert st["max_residue"] <= 1e-6
+    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
+
+
 def fan_in_graph(k=40000, fan=64):
     """k sources s -> 0 and s -> s+1 (chain), plus 0 -> 1..fan: vertex 0's
     seeding residue (R4) is k adds of the same c = (1-a)a/2 onto a sum growing
@@ -392,14 +410,26 @@ def test_pagerank_fp64_seeding(atos, kernel, worker):
     adds measured 1.7e-4 of max x* here, and 4.8e-4 on RMAT-27's hub)."""
     g = fan_in_graph()
     x = oracle.pagerank(g, 0.85)[0]
-    # thread workers also need fp64 residues in the main phase on this graph (the hub's
-    # residue grows while a lane walks its serial list: measured 5.7e-4 with fp32 residues,
-    # fetch 1, discrete; the documented policy of test_pagerank_matrix, R26)
+    # thread and warp workers also need fp64 residues on this graph: the hub's residue
+    # grows while it waits and eps-sized fp32 adds round away (measured 2.2e-4 warp /
+    # persistent, 5.7e-4 thread / discrete; DESIGN R30)
     r, st = atos.pagerank(atos.Graph.from_csr(g), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
-                          cta_threads=T(worker, 32), pr_residue_fp64=worker == "thread")
+                          cta_threads=T(worker, 32), pr_residue_fp64=worker != "cta")
     err = np.max(np.abs(r.astype(np.float64) - x)) / x.max()
     assert err <= PR_TOL, err
     assert st["max_residue"] <= 1e-6
+
+
+@pytest.mark.parametrize("kernel", ["persistent", "discrete"])
+@pytest.mark.parametrize("worker", WORKERS)
+def test_pagerank_fp32_loss_is_one_sided(atos, kernel, worker):
+    """With fp32 residues the fan-in hub can only lose mass (pushes that round
+    away): rank <= x* (the P:481-540 invariant with dropped pushes)."""
+    g = fan_in_graph()
+    x = oracle.pagerank(g, 0.85)[0]
+    r, _ = atos.pagerank(atos.Graph.from_csr(g), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
+                         cta_threads=T(worker, 32))
+    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
 
 
 @pytest.mark.parametrize("check_size", [1, 8, 32])
