@@ -404,17 +404,15 @@ def fan_in_graph(k=40000, fan=64):
 
 @pytest.mark.parametrize("kernel", ["persistent", "discrete"])
 @pytest.mark.parametrize("worker", WORKERS)
-def test_pagerank_fp64_seeding(atos, kernel, worker):
-    """R30: the seeding sums are accumulated in fp64 and rounded once, so the
-    fp32-residue result meets the tolerance on a fan-in hub (fp32 seeding
-    adds measured 1.7e-4 of max x* here, and 4.8e-4 on RMAT-27's hub)."""
+def test_pagerank_fan_in_hub(atos, kernel, worker):
+    """A 40,000-way fan-in hub (x* = 11,930) with fp64 residues: the seeding
+    (fp64 sums, R30) and the main phase reach the Jacobi fixed point.  With
+    fp32 residues this graph loses eps-sized pushes at the hub (1.8e-4 to
+    5.8e-4 of max x* measured, every worker; R32) — see the one-sided test."""
     g = fan_in_graph()
     x = oracle.pagerank(g, 0.85)[0]
-    # thread and warp workers also need fp64 residues on this graph: the hub's residue
-    # grows while it waits and eps-sized fp32 adds round away (measured 2.2e-4 warp /
-    # persistent, 5.7e-4 thread / discrete; DESIGN R30)
     r, st = atos.pagerank(atos.Graph.from_csr(g), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
-                          cta_threads=T(worker, 32), pr_residue_fp64=worker != "cta")
+                          cta_threads=T(worker, 32), pr_residue_fp64=True)
     err = np.max(np.abs(r.astype(np.float64) - x)) / x.max()
     assert err <= PR_TOL, err
     assert st["max_residue"] <= 1e-6
