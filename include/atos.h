@@ -88,6 +88,10 @@ typedef struct {
                           /*   out-edges and residue < pr_defer_factor * eps is re-queued once   */
                           /*   instead of expanded (R31); 0 = off                                 */
   int32_t pr_defer_factor;
+  int32_t hub_split;      /* persistent CTA workers: split a popped vertex with > 4096 edges into  */
+                          /*   2048-edge chunk tasks (R24).  -1 = app default (BFS on, PageRank  */
+                          /*   off: R33), 0 = off, 1 = on                                         */
+  int32_t _pad0;
 } atos_config;
 
 /* One timeline record per batch processed by a persistent/discrete worker:

@@ -56,7 +56,8 @@ class CConfig(ctypes.Structure):
                 ("queue_capacity", ctypes.c_int64), ("timeout_s", ctypes.c_double),
                 ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64),
                 ("stage_edges", ctypes.c_int32), ("sink_defer", ctypes.c_int32),
-                ("pr_defer_degree", ctypes.c_int32), ("pr_defer_factor", ctypes.c_int32)]
+                ("pr_defer_degree", ctypes.c_int32), ("pr_defer_factor", ctypes.c_int32),
+                ("hub_split", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
 
 
 class CStats(ctypes.Structure):
@@ -142,6 +143,7 @@ class Config:
     sink_defer: bool = True        # never push dangling vertices (BFS: no-op tasks; PR: one final pass) (R29)
     pr_defer_degree: int = 0       # PR hub deferral (R31): min out-degree; 0 = off
     pr_defer_factor: int = 4       # ... defer while residue < factor * eps
+    hub_split: int = -1            # hub chunk tasks (R24): -1 app default (BFS on, PR off, R33), 0 off, 1 on
 
     def to_c(self) -> CConfig:
         c = CConfig()
@@ -164,6 +166,7 @@ class Config:
         c.sink_defer = int(self.sink_defer)
         c.pr_defer_degree = self.pr_defer_degree
         c.pr_defer_factor = self.pr_defer_factor
+        c.hub_split = self.hub_split
         s = self.stream
         if s is None:
             import torch

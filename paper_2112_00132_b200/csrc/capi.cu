@@ -88,6 +88,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->sink_defer = 1;
   c->pr_defer_degree = 0;
   c->pr_defer_factor = 4;
+  c->hub_split = -1;
 }
 
 static atos_status check_config(const atos_config* c) {
@@ -108,6 +109,8 @@ static atos_status check_config(const atos_config* c) {
   if (c->trace && c->trace_capacity < 0) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "trace_capacity < 0");
   if (c->stage_edges < -1 || c->stage_edges > (1 << 20))
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "stage_edges %d not in [-1, 2^20]", c->stage_edges);
+  if (c->hub_split < -1 || c->hub_split > 1)
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "hub_split %d not in {-1, 0, 1}", c->hub_split);
   if (c->pr_activation == 1 && c->check_size < 1)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "check_size < 1");
   return ATOS_OK;
@@ -356,6 +359,7 @@ struct LaunchCtx {
   int64_t launches = 0;       // every kernel launched by the call up to the run's end
   int64_t post_launches = 0;  // launched after the run (reductions, conversions)
   int64_t rounds = 0;
+  bool split = true;  // hub chunk splitting (R24) for persistent CTA edge-map workers
   std::chrono::steady_clock::time_point t0;
 };
 
@@ -397,7 +401,7 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
   auto kern = k_persistent<P, App, W>;
   const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads, P::kWarpSpecialised);
   Queue qq = q;
-  if (W == W_CTA && P::kSplit) {
+  if (W == W_CTA && P::kSplit && c.split) {
     Workspace& w = c.g->ws;
     if (!w.chunks) {
       w.chunk_cap = 1ull << 20;
@@ -720,6 +724,7 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
   c.launches += 2;
   CK(cudaEventRecord(w.ev[1], c.s));
   BfsApp app{w.u32a, w.u32b, w.u16a, c.cfg.bfs_filter, c.cfg.sink_defer ? g->d_sink : nullptr};
+  c.split = c.cfg.hub_split != 0;  // R24: on by default for BFS
   using P = EdgeMapPolicy<BfsApp>;
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
     CKS(run_persistent<P>(c, app, make_queue(g, c.cfg, 0)));
@@ -778,6 +783,7 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
   // R31: hub deferral only where the queue agent runs (persistent CTA workers) and ids leave bit 30 free
   const bool dfr = c.cfg.pr_defer_degree > 0 && c.cfg.kernel == ATOS_KERNEL_PERSISTENT &&
                    c.cfg.worker == ATOS_WORKER_CTA && n <= (int64_t)DEFER_BIT;
+  c.split = c.cfg.hub_split == 1;  // R33: off by default for PageRank
   PrAppT<R> app{rank, res, (R)alpha, (R)eps, sink_bits, dfr ? (uint32_t)c.cfg.pr_defer_degree : 0u,
                 (R)eps * (R)std::max(1, c.cfg.pr_defer_factor)};
   if (c.cfg.pr_activation == 1) {

@@ -426,8 +426,14 @@ constexpr int LBS_UNROLL = 8;
 // parallel instead of one CTA walking it serially while the rest of the GPU
 // speculates on depths the hub has not yet fixed (the measured source of
 // RMAT-24 BFS overwork).
-constexpr int64_t CHUNK_EDGES = 2048;
-constexpr int64_t SPLIT_DEG = 2 * CHUNK_EDGES;
+#ifndef ATOS_CHUNK_EDGES
+#define ATOS_CHUNK_EDGES 2048
+#endif
+#ifndef ATOS_SPLIT_DEG
+#define ATOS_SPLIT_DEG (2 * ATOS_CHUNK_EDGES)
+#endif
+constexpr int64_t CHUNK_EDGES = ATOS_CHUNK_EDGES;
+constexpr int64_t SPLIT_DEG = ATOS_SPLIT_DEG;
 
 template <class P>
 __device__ __forceinline__ uint64_t pack_payload(P p) {
