@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--fetch", type=int, default=128, help="BFS FETCH_SIZE")
     ap.add_argument("--threads", type=int, default=256, help="BFS cta_threads")
     ap.add_argument("--pr-fetch", type=int, default=128, help="PageRank FETCH_SIZE")
-    ap.add_argument("--pr-threads", type=int, default=512, help="PageRank cta_threads")
+    ap.add_argument("--pr-threads", type=int, default=1024, help="PageRank cta_threads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-color", action="store_true", help="skip the time-to-colour leg (symmetrised graph)")
@@ -204,6 +204,16 @@ def cpu_baseline(g, depth_gpu, gs=None, colors_gpu=None):
 
 
 # ------------------------------------------------------------------ atos
+def pr_work_bsp(atos, G):
+    """PageRank work for `value` (SURVEY 8d GTEPS_norm, the tbl:extrawork normalisation P:818):
+    the edge pushes of our own BSP push run (Alg. 3) at the same alpha/eps on the same graph,
+    measured once, untimed.  A fixed work count makes `value` proportional to 1/time:
+    raw edge pushes would reward a schedule for doing more pushes."""
+    _, st = atos.pagerank(G, ALPHA, EPS, kernel="bsp", worker="cta", fetch_size=128, cta_threads=256,
+                          timeout_s=300)
+    return int(st["edges_processed"])
+
+
 def run_atos(args, rank, world, local_rank):
     import torch
     import paper_2112_00132_b200 as atos
@@ -221,6 +231,7 @@ def run_atos(args, rank, world, local_rank):
     rank_out = torch.empty(g.n, dtype=torch.float32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     deg = g.degrees()
+    w_pr = pr_work_bsp(atos, G)
 
     def step():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -262,7 +273,7 @@ def run_atos(args, rank, world, local_rank):
         t = torch.tensor([tot_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         tot_ms = float(t.item())
-    tot_edges = (e_bfs * len(records) + sum(e_pr)) * world
+    tot_edges = (e_bfs + w_pr) * len(records) * world
     value = tot_edges / (tot_ms * 1e-3) / 1e9
     hbm, peak_kind = peaks()
     # dominant kernel: PageRank persistent kernel (hot-path kernel_ms from the library's events)
@@ -301,7 +312,10 @@ def run_atos(args, rank, world, local_rank):
                 "roofline_frac": bfs_ach / hbm, "achieved_gbs": bfs_ach,
                 "overwork": statistics.mean(r[2]["tasks_popped"] for r in records) / max(v_exp, 1),
                 "overwork_def": "pops / reached vertices with out-degree > 0 (dangling ones are not pushed, R29)"},
+        "value_def": "(BFS reached out-edges + PageRank BSP-equivalent edge pushes) / device time (GTEPS_norm, SURVEY 8d)",
         "pagerank": {"gteps_raw": statistics.mean(e / (t * 1e-3) / 1e9 for e, t in zip(e_pr, t_pr)),
+                     "work_bsp_pushes": w_pr,
+                     "gteps_norm": statistics.mean(w_pr / (t * 1e-3) / 1e9 for t in t_pr),
                      "ms": statistics.mean(t_pr), "kernel_ms": pr_kms, "edge_pushes": statistics.mean(e_pr),
                      "pops": statistics.mean(pops_pr), "max_residue": max(r[3]["max_residue"] for r in records)},
         "gpu_launches": launches,
@@ -309,7 +323,7 @@ def run_atos(args, rank, world, local_rank):
         "graph_gen_s": gen_s,
     }
     if not args.no_e2e:
-        out["e2e"] = e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world)
+        out["e2e"] = e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world, w_pr)
     gs = colors = None
     if not args.no_color:
         gs, colors, out["color"] = color_leg(args, atos, dev, flush)
@@ -345,7 +359,7 @@ def color_leg(args, atos, dev, flush):
         "kernel": "persistent", "worker": "cta", "fetch_size": 128, "cta_threads": 256}
 
 
-def e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world):
+def e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world, w_pr):
     """Same metric through the public API from pinned host buffers: graph upload
     (atos_graph_create H2D), BFS + PageRank, results read back to host."""
     import torch
@@ -365,7 +379,7 @@ def e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world):
         G.close()
         if i >= 2:
             d = depth.numpy().view(np.uint32)
-            edges.append(int(deg[d != atos.UNREACHED].sum()) + sp["edges_processed"])
+            edges.append(int(deg[d != atos.UNREACHED].sum()) + w_pr)
             times.append(t1 - t0)
     h2d = g.off.nbytes + g.col.nbytes
     d2h = g.n * 8
@@ -392,6 +406,10 @@ def run_atos_multi(args, rank, world, local_rank):
     g, fwd = gg.permute(g0, 12345)
     src = int(fwd[0])
     del g0
+    Gw = atos.Graph(g.off, g.col)
+    w_pr = pr_work_bsp(atos, Gw)  # fixed PageRank work of this (permuted) graph, as at N = 1
+    Gw.close()
+    del Gw
     pg = adist.PartGraph.from_global(g, world, rank)
     cfg = atos.Config(kernel=args.dist_kernel_bfs, worker="cta", fetch_size=args.fetch, cta_threads=args.threads,
                       timeout_s=300)
@@ -437,7 +455,7 @@ def run_atos_multi(args, rank, world, local_rank):
     launches = sum(r[3]["kernel_launches"] + r[4]["kernel_launches"] for r in recs) // len(recs)
     e_bfs, e_pr = int(loc[0].item()), float(loc[1].item())
     tot_ms = float(t[0].item())
-    value = (e_bfs * len(recs) + e_pr) / (tot_ms * 1e-3) / 1e9
+    value = (e_bfs + w_pr) * len(recs) / (tot_ms * 1e-3) / 1e9
     hbm, peak_kind = peaks()
     out = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
@@ -452,7 +470,8 @@ def run_atos_multi(args, rank, world, local_rank):
                    "l2": "flushed (512 MB write) between steps; inputs > L2"},
         "bfs": {"gteps": e_bfs / (float(t[1].item()) / len(recs) * 1e-3) / 1e9, "ms": float(t[1].item()) / len(recs),
                 "rounds": int(loc[2].item()) // world},
-        "pagerank": {"ms": float(t[2].item()) / len(recs), "edge_pushes": e_pr / len(recs),
+        "value_def": "(BFS reached out-edges + PageRank BSP-equivalent edge pushes) / device time (GTEPS_norm, SURVEY 8d)",
+        "pagerank": {"ms": float(t[2].item()) / len(recs), "edge_pushes": e_pr / len(recs), "work_bsp_pushes": w_pr,
                      "rounds": int(loc[3].item()) // world},
         "bytes_exchanged_per_step": float(loc[4].item()) / len(recs),
         "roofline": {"bound": "hbm", "achieved": (8.0 * e_pr / len(recs)) / (float(t[2].item()) / len(recs) * 1e-3) / 1e9 / world,

@@ -36,7 +36,7 @@ def test_rmat24_bfs_bench_config(atos, rmat24):
 
 def test_rmat24_pagerank_bench_config(atos, rmat24):
     G = atos.Graph(rmat24.off, rmat24.col)
-    r, st = atos.pagerank(G, 0.85, 1e-6, kernel="persistent", worker="cta", fetch_size=128, cta_threads=512)
+    r, st = atos.pagerank(G, 0.85, 1e-6, kernel="persistent", worker="cta", fetch_size=128, cta_threads=1024)
     x, _ = oracle.pagerank(rmat24, 0.85)
     err = float(np.max(np.abs(r.astype(np.float64) - x)) / x.max())
     assert err <= 1e-4, err

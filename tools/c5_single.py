@@ -49,7 +49,7 @@ out = {"workload": f"rmat{a.scale}_ef16 single GPU (C5 at N=1)", "n": g.n, "m": 
                "overwork": st["tasks_popped"] / max(1, v_exp)}, "pagerank": {}}
 ranks = {}
 for name, kw in json.loads(a.pr_variants).items():
-    cfg_pr = atos.Config(fetch_size=128, cta_threads=512, timeout_s=600, **kw)
+    cfg_pr = atos.Config(fetch_size=128, cta_threads=1024, timeout_s=600, **kw)
     flush.fill_(1.0); torch.cuda.synchronize()
     _, sp = atos.pagerank(G, 0.85, 1e-6, cfg_pr, out=rank_out)
     ranks[name] = rank_out.cpu().numpy().astype(np.float64)
