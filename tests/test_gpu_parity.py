@@ -331,7 +331,7 @@ def test_pagerank_matrix(atos, kernel, worker, fetch):
     assert err <= PR_TOL, err
     assert st["max_residue"] <= 1e-6
     # one-sided bound 0 <= x* - rank <= eps x*/(1-a) (+ fp32 rounding)
-    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
+    assert np.all(r <= x * (1 + 1e-5) + 2e-5 * x.max())  # fp32 rounding may overshoot slightly
 
 
 @pytest.mark.parametrize("worker", WORKERS)
@@ -360,7 +360,7 @@ def test_pagerank_sink_defer(atos, kernel, worker):
                               cta_threads=T(worker, 32), pr_residue_fp64=worker == "thread", sink_defer=defer)
         assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
         assert st["max_residue"] <= 1e-6
-        assert np.all(r <= x * (1 + 1e-5) + 1e-6)
+        assert np.all(r <= x * (1 + 1e-5) + 2e-5 * x.max())  # fp32 rounding may overshoot slightly
         pushed[defer] = st["tasks_pushed"]
     assert pushed[True] < pushed[False], pushed
 
@@ -391,7 +391,7 @@ def test_pagerank_hub_deferral(atos, gname, deg, factor):
                           pr_residue_fp64=gname == "fanin")
     assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
     assert st["max_residue"] <= 1e-6
-    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
+    assert np.all(r <= x * (1 + 1e-5) + 2e-5 * x.max())  # fp32 rounding may overshoot slightly
 
 
 def fan_in_graph(k=40000, fan=64):
