@@ -369,7 +369,7 @@ def e2e(args, g, atos, stream, cfg_bfs, cfg_pr, world, w_pr):
     rk = torch.empty(g.n, dtype=torch.float32).pin_memory()
     deg = g.degrees()
     times, edges = [], []
-    for i in range(2 + max(1, args.steps // 2)):
+    for i in range(2 + max(3, args.steps)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         G = atos.Graph(off.numpy(), col.numpy())
