@@ -513,3 +513,27 @@ def test_color_requires_symmetric(atos):
     with pytest.raises(atos.AtosError) as e:
         atos.color(D(atos, "rmat16"))
     assert e.value.name == "INVALID_GRAPH"
+
+
+def test_pool_reuse_across_graphs(atos):
+    """Graph-lifetime arrays come from a retained stream-ordered pool (DESIGN §5
+    Allocation): a destroyed graph's HBM is handed to the next create, so every
+    array must be initialised per call.  Alternate a large and a small graph,
+    destroying each after use, and check exact BFS / PageRank / colouring."""
+    big, small = G("rmat16"), G("grid64")
+    x_big, x_small = jacobi("rmat16"), oracle.pagerank(small, 0.85)[0]
+    for _ in range(3):
+        for g, x in ((big, x_big), (small, x_small)):
+            Gd = atos.Graph.from_csr(g)
+            d, _ = atos.bfs(Gd, 0)
+            assert np.array_equal(d, oracle.bfs(g, 0))
+            r, st = atos.pagerank(Gd, 0.85, 1e-6)
+            assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
+            Gd.close()
+    gs = G("rmat12s")
+    for _ in range(2):
+        Gd = atos.Graph.from_csr(gs, symmetric=True)
+        c, k, _ = atos.color(Gd)
+        bad, kk = oracle.check_coloring(gs, c)
+        assert bad == 0 and kk == k
+        Gd.close()
