@@ -43,7 +43,14 @@ __device__ __forceinline__ void warp_exclusive_scan(int64_t* a, int n) {
 // at a time in phases — slot loads, then every item's begin loads, then every
 // item's begin atomics — so ~3 L2 round trips cover 32*AGENT_G items instead
 // of ~3 per item (the agent warp was the bottleneck on low-degree frontiers).
-constexpr int AGENT_G = 4;
+// AGENT_G sweep on RMAT-24 (tools/gpu_jobs/agentg.sh, 3 alternating reps):
+// PageRank 166.6 / 164.4 / 166.6 / 175.0 ms and BFS 3.51 / 3.46 / 3.48 / 3.63 ms
+// at AGENT_G 4 / 2 / 1 / 8 — two items per lane per phase is the best balance
+// of in-flight L2 requests and agent registers.
+#ifndef ATOS_AGENT_G
+#define ATOS_AGENT_G 2
+#endif
+constexpr int AGENT_G = ATOS_AGENT_G;
 
 // Apps that may defer a popped task (PageRank hub deferral, R31) declare kDefer.
 template <class A, class = void>
