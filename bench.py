@@ -410,7 +410,8 @@ def run_atos_multi(args, rank, world, local_rank):
     w_pr = pr_work_bsp(atos, Gw)  # fixed PageRank work of this (permuted) graph, as at N = 1
     Gw.close()
     del Gw
-    pg = adist.PartGraph.from_global(g, world, rank)
+    comm = adist.Comm.auto()  # NCCL over NVLink/NVSwitch (host callbacks for a gloo group)
+    pg = adist.PartGraph.from_global(g, comm)
     cfg = atos.Config(kernel=args.dist_kernel_bfs, worker="cta", fetch_size=args.fetch, cta_threads=args.threads,
                       timeout_s=300)
     cfg_pr = atos.Config(kernel=args.dist_kernel_pr, worker="cta", fetch_size=args.fetch, cta_threads=args.threads,
@@ -496,7 +497,7 @@ def color_leg_multi(args, rank, world, dev, flush):
     import graphgen as gg
     from paper_2112_00132_b200 import dist as adist
     gs, _ = gg.permute(gg.rmat(args.scale, args.edge_factor, seed=1, symmetrize=True), 12345)
-    pg = adist.PartGraph.from_global(gs, world, rank)
+    pg = adist.PartGraph.from_global(gs, adist.Comm.auto())
     stream = torch.cuda.current_stream()
     ms, k, st = [], 0, {}
     for i in range(4):

@@ -52,7 +52,8 @@ typedef enum { ATOS_WORKER_THREAD = 0, ATOS_WORKER_WARP = 1, ATOS_WORKER_CTA = 2
 /* atos_graph_create flags */
 enum {
   ATOS_GRAPH_DEVICE_PTRS = 1, /* row_offsets / col_indices are device pointers          */
-  ATOS_GRAPH_BORROW = 2,      /* with DEVICE_PTRS: zero-copy, caller keeps them alive    */
+  ATOS_GRAPH_BORROW = 2,      /* with DEVICE_PTRS: zero-copy, caller keeps them alive;   */
+                              /*   the library never writes them (no hub tags, R34)      */
   ATOS_GRAPH_VALIDATE = 4,    /* check off[0]==0, off[n]==m, monotone, cols in range     */
   ATOS_GRAPH_SYMMETRIC = 8    /* caller asserts the graph is undirected (needed by atos_color) */
 };
@@ -131,8 +132,9 @@ void atos_config_default(atos_config* cfg);
 
 /* Build a graph handle from CSR: row_offsets int64[n+1], col_indices int32[m]
  * (P:427 vertex.neighbors; S:26-37 invariants).  Copies to the device unless
- * ATOS_GRAPH_BORROW|ATOS_GRAPH_DEVICE_PTRS.  m may exceed 2^31.  n == 0 is
- * allowed.  Errors: INVALID_ARGUMENT (n<0, m<0, NULL pointers with m>0, out==NULL),
+ * ATOS_GRAPH_BORROW|ATOS_GRAPH_DEVICE_PTRS.  A copied CSR gets hub tags (bit
+ * 31 of a column entry = its target's in-degree is >= 512, R34; internal to
+ * the library).  m may exceed 2^31.  n == 0 is allowed.  Errors: INVALID_ARGUMENT (n<0, m<0, NULL pointers with m>0, out==NULL),
  * UNSUPPORTED (n >= 2^31-1), INVALID_GRAPH (with VALIDATE), OUT_OF_MEMORY, CUDA. */
 atos_status atos_graph_create(const int64_t* row_offsets, const int32_t* col_indices, int64_t n,
                               int64_t m, uint32_t flags, atos_graph* out);
@@ -151,9 +153,15 @@ atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t
 /* Push PageRank (async: Alg. 4; BSP: Alg. 3) with
  * damping alpha (the paper's lambda) and threshold eps: unnormalised ranks,
  * fixed point x = (1-alpha) 1 + alpha P x (R4, R5, R8).  On return every
- * residue is <= eps and 0 <= x^* - rank <= eps x^* / (1-alpha), up to fp32 rounding.
- * rank_out: float[n].  Errors: INVALID_ARGUMENT (alpha not in (0,1), eps <= 0 or
- * NaN), QUEUE_OVERFLOW, TIMEOUT, CUDA. */
+ * residue is <= eps and 0 <= x^* - rank <= eps x^* / (1-alpha), up to the
+ * residues' rounding: fp32 residues, except fp64 at hub vertices (in-degree
+ * >= 512, tagged at graph create, R34) — rounding stays below ~3e-5 of each
+ * rank — or fp64 everywhere with cfg->pr_residue_fp64, on a graph created
+ * with ATOS_GRAPH_BORROW, and on partitioned graphs.  Ranks accumulate in
+ * fp64 and are returned as float.  rank_out: float[n].  Errors:
+ * INVALID_ARGUMENT (alpha not in (0,1), eps <= 0 or NaN), QUEUE_OVERFLOW,
+ * TIMEOUT, CUDA; UNSUPPORTED for Check_Size window activation outside
+ * persistent CTA workers with fp32 residues. */
 atos_status atos_pagerank(atos_graph g, float alpha, float eps, const atos_config* cfg,
                           float* rank_out, atos_stats* stats);
 
@@ -171,61 +179,81 @@ const char* atos_last_error(void);
 const char* atos_version(void);
 
 /* ---------------- multi-GPU (one process per GPU, 1-D vertex partition) ---------------- */
-/* BFS and PageRank shard by a 1-D vertex split (callers permute
- * vertex ids first: a block split of RMAT is 3.4x edge-imbalanced).  Each rank
- * runs the same persistent queue kernel on its own vertices to LOCAL
- * quiescence; activations of remote vertices are batched per round into one
- * message buffer grouped by destination rank; the caller exchanges the buffers
- * with an all-to-all (torch.distributed -> NCCL over NVLink/NVSwitch) and
- * applies what it received; the run ends when a round sends no message on any
- * rank (an all-reduce).  A message is (uint64)(dest_local_id << 32 | payload),
- * payload = BFS depth (u32) or PageRank residue contribution (f32 bits).
- * BFS: a remote vertex is sent at most once per improvement (per-rank
- * sent_min filter).  PageRank: remote contributions are accumulated per
- * destination vertex; a round sends those above eps, and the run closes with
- * a flush-all round (no mass is stranded).  Colouring (app 2, SURVEY §8f row
- * f4; needs ATOS_GRAPH_SYMMETRIC, world <= 64): each rank colours its vertices
- * with Alg. 6 against a replica of all colours; a message is
- * (uint64)(global_id << 32 | colour), sent once per round to every rank owning
- * a neighbour of a vertex whose colour changed; the receiver re-ASSIGNs a
- * local v that now shares a colour with a smaller changed neighbour (R13 across
- * ranks).  The run ends after a round in which no rank sent anything. */
+/* BFS and PageRank shard by a 1-D vertex split — rank r owns the
+ * contiguous global ids [v_begin_r, v_end_r) (callers permute ids first: a
+ * block split of RMAT is 3.4x edge-imbalanced).  atos_bfs / atos_pagerank /
+ * atos_color on a partitioned handle run the WHOLE multi-round computation
+ * inside the library (the worker loop of P:251-256 "until the stop condition",
+ * with remote activations batched per round):
+ *   - each round every rank runs the single-GPU queue kernel on its own
+ *     vertices (persistent: to local quiescence; discrete: one superstep) on
+ *     cfg->stream; updates of remote vertices go to a per-destination outbox;
+ *   - the ranks exchange one round vector each (messages per destination,
+ *     pending local tasks, abort/overflow flags) with an all-gather — the
+ *     round's only host synchronisation — then the messages with an
+ *     all-to-all (NCCL send/recv on device buffers over NVLink/NVSwitch, or the
+ *     host callbacks of atos_comm_init_host), applied by the receiver;
+ *   - a round with no message and no pending task on any rank ends the run
+ *     (PageRank: after one closing round that flushes every remaining remote
+ *     contribution); an error on any rank fails the call on EVERY rank.
+ * Every rank must make the same call (same src / alpha / eps / cfg->kernel).
+ * Messages are (uint64)(dest_local_id << 32 | payload), payload = BFS depth,
+ * PageRank contribution (f32 bits) or colour.  BFS sends a remote vertex once
+ * per improvement (per-rank sent_min filter); PageRank accumulates remote
+ * contributions per destination in fp64 and sends those above eps (R28);
+ * colouring (ATOS_GRAPH_SYMMETRIC, world <= 64) keeps a replica of
+ * all colours and sends a changed colour once per round to every rank owning
+ * a neighbour; the receiver re-ASSIGNs a local v that now shares a colour with
+ * a smaller changed neighbour (R13 across ranks). */
+typedef struct atos_comm_s* atos_comm; /* opaque communicator */
 
-/* Partitioned graph for rank `rank` of `world`: it owns global vertices
- * [bounds[rank], bounds[rank+1]) (bounds: host int64[world+1], bounds[0] = 0,
- * bounds[world] = global_n).  local_row_offsets int64[n_local+1] starting at 0,
- * col_global int32[local_m] global ids.  Copies like atos_graph_create (flags:
- * DEVICE_PTRS / VALIDATE honoured; BORROW ignored). */
-atos_status atos_graph_create_partitioned(int64_t global_n, int32_t world, int32_t rank,
-                                          const int64_t* bounds, const int64_t* local_row_offsets,
-                                          const int32_t* col_global, int64_t local_m, uint32_t flags,
-                                          atos_graph* out);
-/* Start a partitioned run: app 0 = BFS from global vertex src (alpha/eps
- * ignored), app 1 = PageRank(alpha, eps) (src ignored), app 2 = greedy
- * colouring (src/alpha/eps ignored; INVALID_GRAPH without SYMMETRIC).
- * Initialises local state (timed into the first round's stats). */
-atos_status atos_part_begin(atos_graph g, int32_t app, int64_t src, float alpha, float eps,
-                            const atos_config* cfg);
-/* One exchange round: run the local queue kernel — persistent: to local
- * quiescence; discrete (cfg.kernel): one superstep over the current snapshot —
- * then gather the round's outgoing messages.  send_counts: host
- * int64[world + 1]: messages per destination ([rank] is 0) and, at [world],
- * local tasks still queued (0 for persistent).  PageRank sends only remote accumulations above
- * eps unless flush_all != 0 (a closing round: everything is sent); the caller
- * ends a PageRank run only after a flush_all round in which no rank sent. */
-atos_status atos_part_run(atos_graph g, int32_t flush_all, int64_t* send_counts);
-/* Copy the round's messages, grouped by destination rank in rank order, to
- * dst (host or device, capacity cap messages; cap >= sum(send_counts)). */
-atos_status atos_part_pack(atos_graph g, uint64_t* dst, int64_t cap);
-/* Apply received messages (host or device buffer of `count` uint64):
- * BFS atomicMin + push on improvement; PageRank atomicAdd + push on an
- * eps crossing; colouring: ghost colour update, then every local vertex in
- * conflict with a smaller changed ghost is re-ASSIGNed. */
-atos_status atos_part_apply(atos_graph g, const uint64_t* msgs, int64_t count);
-/* Finish: write the local results (BFS: uint32 depth, PageRank: float rank, colouring: int32 colour;
- * n_local = bounds[rank+1]-bounds[rank] entries, host or device) and the
- * accumulated statistics (rounds = exchange rounds; bytes_sent = message bytes). */
-atos_status atos_part_finish(atos_graph g, void* out, atos_stats* stats);
+/* NCCL unique id (128 bytes) for atos_comm_init: one rank creates it and the
+ * caller distributes it to the others.  Errors: NCCL (libnccl.so.2 not
+ * loadable, or NCCL failed). */
+atos_status atos_comm_unique_id(uint8_t id_out[128]);
+/* NCCL communicator of rank `rank` of `world` on the current device (one
+ * process per GPU).  Collective: every rank must call it.  NCCL is loaded at
+ * run time (dlopen "libnccl.so.2": the copy already in the process, e.g.
+ * torch's, if any).  Errors: INVALID_ARGUMENT, NCCL. */
+atos_status atos_comm_init(int32_t rank, int32_t world, const uint8_t id[128], atos_comm* out);
+/* Communicator whose exchanges are done by caller callbacks on HOST memory
+ * (e.g. a gloo process group; the library stages device buffers through
+ * pinned host memory).  Both callbacks are collective over the `world` ranks
+ * and return 0 on success (anything else fails the call with ATOS_ERR_NCCL):
+ *   allgather(user, send, recv, bytes): recv = every rank's `bytes` bytes of
+ *     send, in rank order (world * bytes);
+ *   alltoallv(user, send, send_bytes, recv, recv_bytes): send holds world
+ *     packed segments in rank order, send_bytes[r] of them for rank r; recv
+ *     receives recv_bytes[r] bytes from rank r, packed in rank order. */
+typedef int (*atos_allgather_fn)(void* user, const void* send, void* recv, int64_t bytes);
+typedef int (*atos_alltoallv_fn)(void* user, const void* send, const int64_t* send_bytes, void* recv,
+                                 const int64_t* recv_bytes);
+atos_status atos_comm_init_host(int32_t rank, int32_t world, atos_allgather_fn allgather,
+                                atos_alltoallv_fn alltoallv, void* user, atos_comm* out);
+/* Rank / world of a communicator (either pointer may be NULL). */
+atos_status atos_comm_info(atos_comm c, int32_t* rank, int32_t* world);
+/* Destroy a communicator (after every graph using it is destroyed). */
+atos_status atos_comm_destroy(atos_comm c);
+
+/* This rank's partition: it owns global vertices [v_begin, v_end) of a graph
+ * with global_n vertices.  local_row_offsets int64[v_end - v_begin + 1]
+ * starting at 0, col_global int32[local_m] GLOBAL ids (host or device per
+ * ATOS_GRAPH_DEVICE_PTRS; copied; VALIDATE and SYMMETRIC honoured, BORROW
+ * ignored).  Collective over `c` (the ranks' ranges are all-gathered and must
+ * tile [0, global_n) in rank order, else INVALID_ARGUMENT on every rank).
+ * atos_bfs(src = GLOBAL id), atos_pagerank and atos_color on the handle write
+ * the results of the owned vertices (v_end - v_begin entries); stats->rounds
+ * = exchange rounds, stats->bytes_sent = message bytes this rank sent. */
+atos_status atos_graph_create_partitioned(atos_comm c, int64_t global_n, int64_t v_begin, int64_t v_end,
+                                          const int64_t* local_row_offsets, const int32_t* col_global,
+                                          int64_t local_m, uint32_t flags, atos_graph* out);
+
+/* Graph-lifetime device memory comes from a private stream-ordered pool that
+ * keeps up to 8 GB of freed memory mapped for reuse by the next graph
+ * (DESIGN §5).  atos_pool_trim releases all but keep_bytes of it to the
+ * device; atos_pool_reserved reports what the pool currently holds. */
+atos_status atos_pool_trim(uint64_t keep_bytes);
+atos_status atos_pool_reserved(uint64_t* bytes);
 
 #ifdef __cplusplus
 }

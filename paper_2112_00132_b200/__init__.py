@@ -21,7 +21,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libatos.so")
+# ATOS_LIB selects a tuning variant built by tools/build_variant.py (experiments only; the
+# product library is never overwritten)
+LIB_PATH = os.environ.get("ATOS_LIB") or os.path.join(_HERE, "libatos.so")
 
 # ---- C enums (include/atos.h) ---------------------------------------------
 OK = 0
@@ -35,9 +37,14 @@ UNREACHED = 0xFFFFFFFF
 EXPORTS = [
     "atos_config_default", "atos_graph_create", "atos_graph_destroy", "atos_graph_info", "atos_bfs",
     "atos_pagerank", "atos_color", "atos_status_string", "atos_last_error", "atos_version",
-    "atos_graph_create_partitioned", "atos_part_begin", "atos_part_run", "atos_part_pack", "atos_part_apply",
-    "atos_part_finish",
+    "atos_comm_unique_id", "atos_comm_init", "atos_comm_init_host", "atos_comm_info", "atos_comm_destroy",
+    "atos_graph_create_partitioned", "atos_pool_trim", "atos_pool_reserved",
 ]
+
+# callback types of atos_comm_init_host (include/atos.h)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64))
 
 
 class AtosError(RuntimeError):
@@ -96,15 +103,17 @@ def lib():
         L.atos_status_string.restype = ctypes.c_char_p
         L.atos_last_error.restype = ctypes.c_char_p
         L.atos_version.restype = ctypes.c_char_p
-        L.atos_graph_create_partitioned.argtypes = [i64, i32, i32, vp, vp, vp, i64, u32, ctypes.POINTER(vp)]
-        L.atos_part_begin.argtypes = [vp, i32, i64, ctypes.c_float, ctypes.c_float, cfgp]
-        L.atos_part_run.argtypes = [vp, i32, vp]
-        L.atos_part_pack.argtypes = [vp, vp, i64]
-        L.atos_part_apply.argtypes = [vp, vp, i64]
-        L.atos_part_finish.argtypes = [vp, vp, stp]
+        L.atos_comm_unique_id.argtypes = [vp]
+        L.atos_comm_init.argtypes = [i32, i32, vp, ctypes.POINTER(vp)]
+        L.atos_comm_init_host.argtypes = [i32, i32, ALLGATHER_FN, ALLTOALLV_FN, vp, ctypes.POINTER(vp)]
+        L.atos_comm_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+        L.atos_comm_destroy.argtypes = [vp]
+        L.atos_graph_create_partitioned.argtypes = [vp, i64, i64, i64, vp, vp, i64, u32, ctypes.POINTER(vp)]
+        L.atos_pool_trim.argtypes = [ctypes.c_uint64]
+        L.atos_pool_reserved.argtypes = [ctypes.POINTER(ctypes.c_uint64)]
         for f in ("atos_graph_create", "atos_graph_destroy", "atos_graph_info", "atos_bfs", "atos_pagerank",
-                  "atos_color", "atos_graph_create_partitioned", "atos_part_begin", "atos_part_run",
-                  "atos_part_pack", "atos_part_apply", "atos_part_finish"):
+                  "atos_color", "atos_comm_unique_id", "atos_comm_init", "atos_comm_init_host", "atos_comm_info",
+                  "atos_comm_destroy", "atos_graph_create_partitioned", "atos_pool_trim", "atos_pool_reserved"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -309,4 +318,15 @@ def color(g: Graph, cfg: Config | None = None, device: bool = False, out=None, *
     return col, k.value, st.to_dict()
 
 
-__all__ = ["Graph", "Config", "Trace", "bfs", "pagerank", "color", "AtosError", "lib", "version", "UNREACHED", "EXPORTS"]
+def pool_trim(keep_bytes: int = 0):
+    """Release the library's retained graph memory down to keep_bytes (atos_pool_trim)."""
+    _check(lib().atos_pool_trim(keep_bytes), "atos_pool_trim")
+
+
+def pool_reserved() -> int:
+    v = ctypes.c_uint64()
+    _check(lib().atos_pool_reserved(ctypes.byref(v)), "atos_pool_reserved")
+    return v.value
+
+
+__all__ = ["pool_trim", "pool_reserved", "Graph", "Config", "Trace", "bfs", "pagerank", "color", "AtosError", "lib", "version", "UNREACHED", "EXPORTS"]

@@ -49,32 +49,56 @@ atos_status atos_set_error(atos_status s, const char* fmt, ...) {
   } while (0)
 
 // ------------------------------------------------------------------ HBM pool
-// Graph-lifetime arrays (CSR, queue ring, per-vertex state) come from the
-// device's default stream-ordered memory pool, which keeps up to
-// kPoolRetainBytes of freed HBM mapped: a create/destroy cycle of the same
-// graph (the e2e loop, a serving process) reuses it instead of paying
-// cudaMalloc/cudaFree (measured 24-100 ms per RMAT-24 create).  Allocation is
-// ordered on the legacy stream and completed before return; frees wait for the
-// device first (as cudaFree does), so the caller's streams see plain memory.
+// Graph-lifetime arrays (CSR, queue ring, per-vertex state) come from a
+// PRIVATE stream-ordered memory pool per device (cudaMemPoolCreate) that keeps
+// up to kPoolRetainBytes of freed HBM mapped: a create/destroy cycle of the
+// same graph (the e2e loop, a serving process) reuses it instead of paying
+// cudaMalloc/cudaFree (measured 24-100 ms per RMAT-24 create).  The device's
+// default pool — shared with every other library in the process — is left
+// alone, and atos_pool_trim() hands retained memory back.  Allocations and
+// frees are ordered on a library-owned stream: an allocation is completed
+// before it is returned (so any caller stream may use it); a free needs no
+// wait, because every entry point is synchronous — no work on the array is
+// outstanding when a handle is destroyed or a workspace regrows.
 static constexpr uint64_t kPoolRetainBytes = 8ull << 30;
 
-static cudaError_t pool_malloc(void** p, size_t bytes) {
-  static bool configured[64] = {};
+struct DevPool {
+  cudaMemPool_t pool = nullptr;
+  cudaStream_t stream = nullptr;
+};
+
+static cudaError_t dev_pool(DevPool** out) {
+  static DevPool pools[64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = kPoolRetainBytes;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    (void)cudaGetLastError();
-    configured[dev] = true;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  DevPool& d = pools[dev];
+  if (!d.pool) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if ((e = cudaMemPoolCreate(&pool, &props)) != cudaSuccess) return e;
+    uint64_t thr = kPoolRetainBytes;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaStream_t s = nullptr;
+    if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    d.stream = s;
+    d.pool = pool;
   }
-  e = cudaMallocAsync(p, bytes, cudaStreamLegacy);
+  *out = &d;
+  return cudaSuccess;
+}
+
+static cudaError_t pool_malloc(void** p, size_t bytes) {
+  DevPool* d = nullptr;
+  cudaError_t e = dev_pool(&d);
   if (e != cudaSuccess) return e;
-  return cudaStreamSynchronize(cudaStreamLegacy);
+  e = cudaMallocFromPoolAsync(p, bytes, d->pool, d->stream);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(d->stream);
 }
 
 template <class T>
@@ -82,8 +106,35 @@ static cudaError_t pool_malloc(T** p, size_t bytes) { return pool_malloc(reinter
 
 static void pool_free(void* p) {
   if (!p) return;
-  cudaDeviceSynchronize();
-  cudaFreeAsync(p, cudaStreamLegacy);
+  DevPool* d = nullptr;
+  if (dev_pool(&d) == cudaSuccess) cudaFreeAsync(p, d->stream);
+  (void)cudaGetLastError();
+}
+
+extern "C" atos_status atos_pool_trim(uint64_t keep_bytes) {
+  DevPool* d = nullptr;
+  cudaError_t e = dev_pool(&d);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+  if (e == cudaSuccess) e = cudaMemPoolTrimTo(d->pool, (size_t)keep_bytes);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return atos_set_error(ATOS_ERR_CUDA, "atos_pool_trim: %s", cudaGetErrorString(e));
+  }
+  return ATOS_OK;
+}
+
+extern "C" atos_status atos_pool_reserved(uint64_t* bytes) {
+  if (!bytes) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "bytes == NULL");
+  DevPool* d = nullptr;
+  cudaError_t e = dev_pool(&d);
+  uint64_t v = 0;
+  if (e == cudaSuccess) e = cudaMemPoolGetAttribute(d->pool, cudaMemPoolAttrReservedMemCurrent, &v);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return atos_set_error(ATOS_ERR_CUDA, "atos_pool_reserved: %s", cudaGetErrorString(e));
+  }
+  *bytes = v;
+  return ATOS_OK;
 }
 
 extern "C" const char* atos_status_string(atos_status s) {
@@ -244,6 +295,27 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
   // dangling-vertex bitmap (R29): a property of the immutable CSR, like the max degree
   CK(pool_malloc(&g->d_sink, (size_t)std::max<int64_t>(1, (n + 31) / 32) * sizeof(uint32_t)));
   if (n) k_sink_bitmap<<<grid_for(n, 256, g->sms), 256>>>(g->d_off, n, g->d_sink);
+  // Hub tags (R34): a library-owned CSR of a whole graph gets bit 31 set on
+  // every column entry whose target has in-degree >= HUB_IN_DEG, plus a hub
+  // bitmap.  (Borrowed columns are the caller's and partitioned graphs only
+  // know local edges: neither is tagged, and PageRank keeps fp64 residues.)
+  if (g->owned && col_bound == n && m > 0) {
+    uint32_t* indeg = nullptr;
+    CK(pool_malloc(&indeg, (size_t)n * sizeof(uint32_t)));
+    CK(cudaMemset(indeg, 0, (size_t)n * sizeof(uint32_t)));
+    k_in_degree<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, indeg);
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g->d_scratch) + 4;
+    CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
+    CK(pool_malloc(&g->d_hub, (size_t)((n + 31) / 32) * sizeof(uint32_t)));
+    k_hub_bitmap<<<grid_for(n, 256, g->sms), 256>>>(indeg, n, HUB_IN_DEG, g->d_hub, cnt);
+    unsigned long long hubs = 0;
+    CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
+    g->num_hubs = (int64_t)hubs;
+    if (hubs) k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, indeg, HUB_IN_DEG);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    pool_free(indeg);
+  }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return ATOS_OK;
@@ -257,6 +329,7 @@ static void graph_free(atos_graph g) {
   }
   cudaFree(g->d_scratch);
   pool_free(g->d_sink);
+  pool_free(g->d_hub);
   Workspace& w = g->ws;
   pool_free(w.ring);
   cudaFree(w.ctl);
@@ -369,7 +442,6 @@ static Queue make_queue(atos_graph g, const atos_config& cfg, uint32_t kind) {
   q.head_floor = 0;
   q.trace_kind = kind;
   q.backoff_ns = 256;
-  if (const char* e = getenv("ATOS_BACKOFF_NS")) q.backoff_ns = (uint32_t)atoi(e);  // tuning experiments only
   q.trace = reinterpret_cast<TraceRec*>(cfg.trace);
   q.trace_cap = cfg.trace ? (uint64_t)cfg.trace_capacity : 0;
   return q;
@@ -421,9 +493,8 @@ static int clamp_threads(int W, int F, int T, bool ws = false) {
 // Staged column elements per batch buffer: `req` (>0: as requested, -1: auto)
 // rounded to a multiple of 4, bounded so per_sm CTAs still fit in the SM's
 // shared memory with `l1_keep` bytes left to L1 (the BFS probes and PR
-// residue atomics go through it).  ATOS_STAGE_EDGES overrides (experiments).
+// residue atomics go through it).
 static int stage_capacity(int req, int per_sm, size_t base_smem) {
-  if (const char* e = getenv("ATOS_STAGE_EDGES")) req = atoi(e);
   if (req == 0) return 0;
   const size_t sm_total = 228 * 1024, per_block_reserved = 1024, l1_keep = 64 * 1024;
   const size_t budget = (sm_total - l1_keep) / (size_t)per_sm;
@@ -439,14 +510,18 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
   auto kern = k_persistent<P, App, W>;
   const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads, P::kWarpSpecialised);
   Queue qq = q;
-  if (W == W_CTA && P::kSplit && c.split) {
+  // R24 hub chunk tasks: only if some vertex is a hub; the table has one
+  // 16-B entry per ring slot (device.cuh, Chunk), so it cannot overflow
+  if (W == W_CTA && P::kSplit && c.split && c.g->max_degree > SPLIT_DEG) {
     Workspace& w = c.g->ws;
-    if (!w.chunks) {
-      w.chunk_cap = 1ull << 20;
-      CK(pool_malloc(&w.chunks, w.chunk_cap * sizeof(Chunk)));
+    if (w.chunk_cap != w.cap) {
+      pool_free(w.chunks);
+      w.chunks = nullptr;
+      w.chunk_cap = 0;
+      CK(pool_malloc(&w.chunks, w.cap * sizeof(Chunk)));
+      w.chunk_cap = w.cap;
     }
     qq.chunks = w.chunks;
-    qq.chunk_mask = w.chunk_cap - 1;
   }
   size_t smem = worker_smem_bytes<P>(W, F, T, true);
   if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
@@ -532,7 +607,7 @@ static atos_status run_discrete_w(LaunchCtx& c, const App& app, Queue q, uint64_
 // WHILE node repeats {one round over [h, t) with a fixed grid, round-end
 // kernel that advances [h, t) and sets the condition}.
 template <class P, class App, int W>
-static atos_status run_discrete_graph_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0) {
+static atos_status run_discrete_graph_w(LaunchCtx& c, const App& app, Queue q, uint64_t t0, uint64_t* h_end) {
   auto kern = k_discrete_dev<P, App, W>;
   const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads);
   const size_t smem = worker_smem_bytes<P>(W, F, T);
@@ -606,6 +681,7 @@ static atos_status run_discrete_graph_w(LaunchCtx& c, const App& app, Queue q, u
     CK(cudaStreamSynchronize(c.s));
     c.rounds += (int64_t)r1.rounds;
     c.launches += 2 * (int64_t)r1.rounds;
+    if (h_end) *h_end = r1.h;
   }
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
@@ -617,9 +693,9 @@ static atos_status run_discrete(LaunchCtx& c, const App& app, const Queue& q, ui
                                 int64_t max_rounds = -1, uint64_t* h_end = nullptr) {
   if (c.cfg.device_loop && max_rounds < 0 && h0 == 0) {
     switch (c.cfg.worker) {
-      case ATOS_WORKER_THREAD: return run_discrete_graph_w<P, App, W_THREAD>(c, app, q, t0);
-      case ATOS_WORKER_WARP: return run_discrete_graph_w<P, App, W_WARP>(c, app, q, t0);
-      default: return run_discrete_graph_w<P, App, W_CTA>(c, app, q, t0);
+      case ATOS_WORKER_THREAD: return run_discrete_graph_w<P, App, W_THREAD>(c, app, q, t0, h_end);
+      case ATOS_WORKER_WARP: return run_discrete_graph_w<P, App, W_WARP>(c, app, q, t0, h_end);
+      default: return run_discrete_graph_w<P, App, W_CTA>(c, app, q, t0, h_end);
     }
   }
   switch (c.cfg.worker) {
@@ -734,12 +810,18 @@ static atos_status begin_call(atos_graph g, const atos_config* cfg_in, LaunchCtx
 }
 
 // ------------------------------------------------------------------ BFS
-atos_status bfs_local(LaunchCtx& c, int64_t src, const atos_config& cfg);
+// partitioned graphs (dist_impl.cuh): the whole multi-round run
+static atos_status part_call(LaunchCtx& c, int app, int64_t src, float alpha, float eps, void* out,
+                             int32_t* ncolors_out, atos_stats* st);
 
 extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t* depth_out, atos_stats* st) {
   LaunchCtx c;
   CKS(begin_call(g, cfg, c, st));
-  if (g->dist) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "partitioned graph: use atos_part_*");
+  if (g->dist) {
+    if (src < 0 || src >= g->global_n)
+      return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "src %lld not in [0, %lld)", (long long)src, (long long)g->global_n);
+    return part_call(c, 0, src, 0.f, 0.f, depth_out, nullptr, st);
+  }
   const int64_t n = g->n;
   if (n == 0) return ATOS_OK;
   if (src < 0 || src >= n) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "src %lld not in [0, %lld)", (long long)src, (long long)n);
@@ -788,8 +870,10 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
 }
 
 // ------------------------------------------------------------------ PageRank
+// rs: residue storage (R34) — fp32 with fp64 hubs (res64 = the seeding sums
+// array) on a tagged graph, or all-fp64 (R = double).
 template <class R>
-static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha, float eps) {
+static atos_status pagerank_run(LaunchCtx& c, Residues<R> rs, double* rank, float alpha, float eps) {
   atos_graph g = c.g;
   Workspace& w = g->ws;
   const int64_t n = g->n;
@@ -797,9 +881,9 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
   CK(cudaEventRecord(w.ev[0], c.s));
   // a2: rank = 1 - alpha ; residue seeded by one synchronous push (R4) ; all vertices enqueued
   k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rank, n, 1.0 - (double)alpha);
-  // R30: the seeding sums accumulate in fp64 (w.f64b; the residue array itself when R = double)
-  // and are rounded once to R: fp32 adds of one repeated c = (1-a)a/deg(v) onto a hub's growing sum
-  // round with correlated errors (measured: RMAT-27's hub 4.8e-4 of max x* low, a fan-in test graph 1.7e-4)
+  // R30: the seeding sums accumulate in fp64 (w.f64b: the hub residues, or every residue when R = double)
+  // and are rounded once to fp32 for non-hubs: fp32 adds of one repeated c = (1-a)a/deg(v) onto a hub's
+  // growing sum round with correlated errors (measured: RMAT-27's hub 4.8e-4 of max x* low)
   double* acc = w.f64b;
   k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, n, 0.0);
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
@@ -810,25 +894,26 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
     CKS((bsp_step_w<EdgeMapPolicy<PrInitAppT<double>>, PrInitAppT<double>, W_CTA>(ci, ia, nullptr, (uint64_t)n,
                                                                                  nullptr, nullptr, 256, nullptr)));
   }
-  if (!std::is_same<R, double>::value) k_f64_to_res<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, res, n);
+  const bool f32 = !std::is_same<R, double>::value;
+  if (f32) k_f64_to_res<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, rs.res, rs.hub, n);
   if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
   // R29: sink deferral for the threshold-activated queue strategies
   const bool sinks = c.cfg.sink_defer && !bsp && c.cfg.pr_activation == 0;
   const uint32_t* sink_bits = sinks ? g->d_sink : nullptr;
   CK(cudaGetLastError());
-  c.launches += (bsp ? 4 : 5) + (std::is_same<R, double>::value ? 0 : 1);
+  c.launches += (bsp ? 4 : 5) + (f32 ? 1 : 0);
   CK(cudaEventRecord(w.ev[1], c.s));
   // R31: hub deferral only where the queue agent runs (persistent CTA workers) and ids leave bit 30 free
   const bool dfr = c.cfg.pr_defer_degree > 0 && c.cfg.kernel == ATOS_KERNEL_PERSISTENT &&
                    c.cfg.worker == ATOS_WORKER_CTA && n <= (int64_t)DEFER_BIT;
   c.split = c.cfg.hub_split == 1;  // R33: off by default for PageRank
-  PrAppT<R> app{rank, res, (R)alpha, (R)eps, sink_bits, dfr ? (uint32_t)c.cfg.pr_defer_degree : 0u,
+  PrAppT<R> app{rank, rs, (R)alpha, (R)eps, sink_bits, dfr ? (uint32_t)c.cfg.pr_defer_degree : 0u,
                 (R)eps * (R)std::max(1, c.cfg.pr_defer_factor)};
   if (c.cfg.pr_activation == 1) {
     if constexpr (std::is_same<R, float>::value) {
       // f1: Alg. 4's Check_Size window activation; every vertex starts queued
       k_fill<uint32_t><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, n, 1u);
-      PrWindowAppT<float> wapp{rank, res, w.u32a, alpha, eps, n, c.cfg.check_size};
+      PrWindowAppT<float> wapp{rank, rs, w.u32a, alpha, eps, n, c.cfg.check_size};
       CKS(run_persistent<EdgeMapPolicy<PrWindowAppT<float>>>(c, wapp, make_queue(g, c.cfg, 1)));
       return ATOS_OK;
     }
@@ -839,7 +924,7 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
     else
       CKS(run_discrete<EdgeMapPolicy<PrAppT<R>>>(c, app, make_queue(g, c.cfg, 1), (uint64_t)n));
     if (sinks) {
-      k_pr_absorb_sinks<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(sink_bits, res, rank, n);
+      k_pr_absorb_sinks<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(sink_bits, rs, rank, n);
       CK(cudaGetLastError());
       c.launches++;
     }
@@ -852,7 +937,7 @@ static atos_status pagerank_run(LaunchCtx& c, R* res, double* rank, float alpha,
     while (cnt > 0) {
       CKS(bsp_step<EdgeMapPolicy<PrBspAppT<R>>>(c, bapp, in, cnt, nullptr, nullptr));
       CK(cudaMemsetAsync(w.fcount, 0, sizeof(unsigned long long), c.s));
-      k_pr_filter<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(res, n, (R)eps, w.front[cur], w.fcount);
+      k_pr_filter<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rs, n, (R)eps, w.front[cur], w.fcount);
       CK(cudaGetLastError());
       c.launches++;
       CKS(bsp_read_count(c, w.fcount, cnt));
@@ -869,17 +954,23 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   CKS(begin_call(g, cfg, c, st));
   if (!(alpha > 0.f && alpha < 1.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "alpha not in (0,1)");
   if (!(eps > 0.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "eps <= 0 or NaN");
-  if (g->dist) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "partitioned graph: use atos_part_*");
+  if (g->dist) {
+    if (c.cfg.pr_activation == 1)
+      return atos_set_error(ATOS_ERR_UNSUPPORTED, "Check_Size window activation is not built for partitioned graphs");
+    return part_call(c, 1, 0, alpha, eps, rank_out, nullptr, st);
+  }
   const int64_t n = g->n;
   if (n == 0) return ATOS_OK;
   if (!rank_out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "rank_out == NULL");
   if (c.cfg.pr_activation == 1 && (c.cfg.kernel != ATOS_KERNEL_PERSISTENT || c.cfg.worker != ATOS_WORKER_CTA ||
-                                   c.cfg.pr_residue_fp64))
+                                   c.cfg.pr_residue_fp64 || !g->d_hub))
     return atos_set_error(ATOS_ERR_UNSUPPORTED,
-                          "Check_Size window activation is built for persistent CTA workers with fp32 residues");
+                          "Check_Size window activation is built for persistent CTA workers with fp32 residues "
+                          "(a library-owned CSR)");
   Workspace& w = g->ws;
   const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
-  const bool r64 = c.cfg.pr_residue_fp64 != 0;
+  // R34: fp32 residues need the hub tags; an untagged (borrowed) graph keeps every residue in fp64
+  const bool r64 = c.cfg.pr_residue_fp64 != 0 || !g->d_hub;
   // at most 2 live copies per vertex (initial + one threshold crossing)
   CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)n, !bsp, c.s));
   if (!bsp && (uint64_t)n > w.cap)
@@ -888,22 +979,24 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   CKS(ensure(w.f32a, w.f32a_n, (size_t)n));
   CKS(ensure(w.f64a, w.f64a_n, (size_t)n));
   if (c.cfg.pr_activation == 1) CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // queued flags
-  CKS(ensure(w.f64b, w.f64b_n, (size_t)n));  // fp64 residues, or the fp64 seeding accumulator (R30)
+  CKS(ensure(w.f64b, w.f64b_n, (size_t)n));  // fp64 residues (all, or the hubs') = the seeding sums (R30)
   if (!r64) CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
   if (bsp) {
     CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
     CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
   }
   double* rank = w.f64a;
-  if (r64) CKS(pagerank_run<double>(c, w.f64b, rank, alpha, eps));
-  else CKS(pagerank_run<float>(c, w.f32b, rank, alpha, eps));
+  const Residues<double> rs64{w.f64b, nullptr, nullptr};
+  const Residues<float> rs32{w.f32b, w.f64b, g->d_hub};
+  if (r64) CKS(pagerank_run<double>(c, rs64, rank, alpha, eps));
+  else CKS(pagerank_run<float>(c, rs32, rank, alpha, eps));
   c.post_launches = st ? 2 : 1;
   CKS(finish_stats(c, st, bsp));
   if (st) {
     unsigned int* mb = reinterpret_cast<unsigned int*>(g->d_scratch) + 8;
     CK(cudaMemsetAsync(mb, 0, sizeof(unsigned int), c.s));
-    if (r64) k_max_f32<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.f64b, n, mb);
-    else k_max_f32<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.f32b, n, mb);
+    if (r64) k_max_res<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rs64, n, mb);
+    else k_max_res<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rs32, n, mb);
     unsigned int hb = 0;
     CK(cudaMemcpyAsync(&hb, mb, sizeof hb, cudaMemcpyDeviceToHost, c.s));
     CK(cudaStreamSynchronize(c.s));
@@ -923,11 +1016,11 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
                                   atos_stats* st) {
   LaunchCtx c;
   CKS(begin_call(g, cfg, c, st));
-  if (g->dist) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "partitioned graph: use atos_part_begin(app = 2)");
   if (!g->symmetric) return atos_set_error(ATOS_ERR_INVALID_GRAPH, "atos_color needs ATOS_GRAPH_SYMMETRIC");
   if (c.cfg.gc_literal) return atos_set_error(ATOS_ERR_UNSUPPORTED, "paper-literal colouring (livelocks, R13) not built");
-  const int64_t n = g->n;
   if (ncolors_out) *ncolors_out = 0;
+  if (g->dist) return part_call(c, 2, 0, 0.f, 0.f, color_out, ncolors_out, st);
+  const int64_t n = g->n;
   if (n == 0) return ATOS_OK;
   if (!color_out) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "color_out == NULL");
   Workspace& w = g->ws;

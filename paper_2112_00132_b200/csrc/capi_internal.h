@@ -25,7 +25,7 @@ struct Workspace {
   size_t f32b_n = 0;
   double* f64a = nullptr;  // PR rank (fp64 accumulation)
   size_t f64a_n = 0;
-  double* f64b = nullptr;  // PR residue when pr_residue_fp64
+  double* f64b = nullptr;  // PR: fp64 residues (all with pr_residue_fp64 / untagged graphs; hubs otherwise, R34)
   size_t f64b_n = 0;
   uint32_t* front[2] = {nullptr, nullptr};
   size_t front_n[2] = {0, 0};
@@ -46,6 +46,8 @@ struct atos_graph_s {
   int32_t* d_col = nullptr;
   int64_t col_cap = 0;  // readable elements of d_col
   uint32_t* d_sink = nullptr;  // bit v = (deg(v) == 0), built at create (R29)
+  uint32_t* d_hub = nullptr;   // bit v = in-degree >= HUB_IN_DEG; columns carry HUB_TAG (R34); nullptr = untagged
+  int64_t num_hubs = 0;
   void* d_scratch = nullptr;
   bool owned = false;
   bool symmetric = false;

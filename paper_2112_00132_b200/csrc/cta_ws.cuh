@@ -58,6 +58,38 @@ struct DeferTrait : std::false_type {};
 template <class A>
 struct DeferTrait<A, std::void_t<decltype(A::kDefer)>> : std::integral_constant<bool, A::kDefer> {};
 
+// Per-item state of a batch between the agent's phases, kept in pre[i]:
+// a vertex item (>= 0, may carry DEFER_BIT), a resolved chunk task
+// (-2 - edges), an item lost to an abort (-1), or not yet read (PENDING).
+constexpr int64_t STASH_PENDING = -0x7fffffffffffffffLL - 1;
+constexpr int64_t STASH_INVALID = -1;
+
+// Take the item of claimed position pos from its slot word `raw` if it is
+// full.  A chunk task is resolved on the spot — its table entry is read while
+// the slot is still held, then the slot is released with st.release (device.cuh,
+// Chunk) — a vertex item is stashed and its slot released.  Returns false if
+// the slot is not published yet.
+template <class App>
+__device__ __forceinline__ bool agent_take(const App& app, const Queue& q, uint64_t pos, uint64_t raw, uint32_t i,
+                                           int64_t* e0s, int64_t* pre, typename App::Payload* pay) {
+  const uint32_t want = 2u * (uint32_t)(pos >> q.log2cap) + 1u;
+  if ((uint32_t)(raw >> 32) != want) return false;
+  const uint32_t it = (uint32_t)raw;
+  if (q.chunks && (it & CHUNK_BIT)) {
+    int64_t a = 0, z = 0;
+    typename App::Payload p{};
+    const bool cur = read_chunk(app, q, pos, a, z, p);
+    e0s[i] = a;
+    pay[i] = p;
+    pre[i] = -2 - (cur ? z - a : 0);
+    q_release_slot_ordered(q, pos);
+  } else {
+    pre[i] = (int64_t)it;
+    q_release_slot(q, pos);
+  }
+  return true;
+}
+
 // Returns the tasks the agent re-pushed (deferred, R31; warp-uniform).
 template <class App>
 __device__ __forceinline__ uint32_t agent_prepare(const App& app, const GraphView& g, const Queue& q, const Queue* cq,
@@ -68,10 +100,15 @@ __device__ __forceinline__ uint32_t agent_prepare(const App& app, const GraphVie
   constexpr bool kDefer = DeferTrait<App>::value;
   const uint32_t lane = lane_id();
   uint32_t deferred = 0;
+  // phase 0: read and release EVERY claimed slot before this agent pushes
+  // anything (hub chunk tasks, deferrals), and never hold a published slot
+  // while spinning on an unpublished one (the batch is re-scanned with backoff
+  // until every item is in).  So a producer waiting for one of these slots to
+  // be released for its next lap (ring wrap-around) never waits on this agent
+  // (the agent used to push between sub-rounds of unread claims).
+  bool pending = false;
   for (uint32_t base = 0; base < n; base += 32 * AGENT_G) {
-    uint32_t it[AGENT_G];
     uint64_t raw[AGENT_G];
-    // phase A: all slot loads in flight, then resolve (spin) any in-flight stores
 #pragma unroll
     for (int k = 0; k < AGENT_G; ++k) {
       const uint32_t i = base + lane + 32 * k;
@@ -80,33 +117,46 @@ __device__ __forceinline__ uint32_t agent_prepare(const App& app, const GraphVie
 #pragma unroll
     for (int k = 0; k < AGENT_G; ++k) {
       const uint32_t i = base + lane + 32 * k;
-      it[k] = 0xFFFFFFFFu;
-      if (i < n) {
-        const uint64_t p = first + i;
-        const uint32_t want = 2u * (uint32_t)(p >> q.log2cap) + 1u;
-        if ((uint32_t)(raw[k] >> 32) == want) {
-          it[k] = (uint32_t)raw[k];
-          st_stream_u64(q.ring + (p & q.mask), (uint64_t)(want + 1u) << 32);
-        } else if (!q_load_slot(q, p, it[k])) {
-          it[k] = 0xFFFFFFFFu;
-        }
+      if (i < n && !agent_take(app, q, first + i, raw[k], i, e0s, pre, pay)) {
+        pre[i] = STASH_PENDING;
+        pending = true;
       }
     }
-    // phase B: begin loads (chunk entries or per-vertex state)
+  }
+  for (unsigned ns = 16; __any_sync(FULL_MASK, pending); ns = ns < 256 ? ns * 2 : ns) {
+    const bool dead = q_aborted(q) || q_timed_out(q);
+    pending = false;
+    if (!dead) __nanosleep(ns);
+    for (uint32_t i = lane; i < n; i += 32) {
+      if (pre[i] != STASH_PENDING) continue;
+      if (dead) { pre[i] = STASH_INVALID; continue; }
+      if (!agent_take(app, q, first + i, ld_relaxed_u64(q.ring + ((first + i) & q.mask)), i, e0s, pre, pay))
+        pending = true;
+    }
+  }
+  __syncwarp();
+  for (uint32_t base = 0; base < n; base += 32 * AGENT_G) {
+    int64_t sv[AGENT_G];
+    uint32_t it[AGENT_G];
+#pragma unroll
+    for (int k = 0; k < AGENT_G; ++k) {
+      const uint32_t i = base + lane + 32 * k;
+      sv[k] = i < n ? pre[i] : STASH_INVALID;
+      it[k] = sv[k] >= 0 ? (uint32_t)sv[k] : 0xFFFFFFFFu;
+    }
+    // phase B: begin loads (per-vertex state)
     Pre x[AGENT_G];
-    bool is_chunk[AGENT_G];
     bool was_deferred[AGENT_G];
 #pragma unroll
     for (int k = 0; k < AGENT_G; ++k) {
-      is_chunk[k] = cq && it[k] != 0xFFFFFFFFu && (it[k] & CHUNK_BIT);
       was_deferred[k] = false;
       if constexpr (kDefer) {
-        if (app.defer_deg && it[k] != 0xFFFFFFFFu && !is_chunk[k] && (it[k] & DEFER_BIT)) {
+        if (app.defer_deg && it[k] != 0xFFFFFFFFu && (it[k] & DEFER_BIT)) {
           was_deferred[k] = true;
           it[k] &= ~DEFER_BIT;
         }
       }
-      if (it[k] != 0xFFFFFFFFu && !is_chunk[k]) x[k] = app.begin_load(it[k], g);
+      if (it[k] != 0xFFFFFFFFu) x[k] = app.begin_load(it[k], g);
     }
     bool dpush[AGENT_G];
     uint32_t ditem[AGENT_G];
@@ -115,32 +165,32 @@ __device__ __forceinline__ uint32_t agent_prepare(const App& app, const GraphVie
       dpush[k] = false;
       ditem[k] = 0;
     }
-    // phase C: commits, chunk handling, splitting; write the batch
+    // phase C: commits and splitting; write the batch
 #pragma unroll
     for (int k = 0; k < AGENT_G; ++k) {
       const uint32_t i = base + lane + 32 * k;
       if (i >= n) continue;
+      if (sv[k] < STASH_INVALID) {  // chunk task, resolved in phase 0
+        pre[i] = -2 - sv[k];
+        continue;
+      }
       int64_t a = 0, z = 0;
       Payload p{};
       bool ok = false;
       if (it[k] != 0xFFFFFFFFu) {
-        if (is_chunk[k]) {
-          ok = prepare_item(app, g, cq, it[k], a, z, p);
-        } else {
-          a = x[k].e0;
-          z = x[k].e1;
-          bool held = false;
-          if constexpr (kDefer) {
-            if (!was_deferred[k] && app.should_defer(x[k])) {
-              held = true;  // residue put back; re-pushed with DEFER_BIT unless another copy exists
-              dpush[k] = app.put_back(it[k], x[k]);
-              ditem[k] = it[k] | DEFER_BIT;
-            }
+        a = x[k].e0;
+        z = x[k].e1;
+        bool held = false;
+        if constexpr (kDefer) {
+          if (!was_deferred[k] && app.should_defer(x[k])) {
+            held = true;  // residue put back; re-pushed with DEFER_BIT unless another copy exists
+            dpush[k] = app.put_back(it[k], x[k]);
+            ditem[k] = it[k] | DEFER_BIT;
           }
-          if (!held) {
-            ok = app.begin_commit(it[k], x[k], p);
-            if (ok && cq && z - a > SPLIT_DEG) z = split_hub(cq, it[k], a, z, p);
-          }
+        }
+        if (!held) {
+          ok = app.begin_commit(it[k], x[k], p);
+          if (ok && cq && z - a > SPLIT_DEG) z = split_hub(cq, it[k], a, z, p);
         }
       }
       e0s[i] = a;
@@ -209,10 +259,7 @@ __device__ __forceinline__ uint32_t window_pop(const App& app, const Queue& q, u
       for (int64_t b = 0; b < app.n; b += 32) {
         const int64_t v = b + lane_id();
         bool act = false;
-        if (v < app.n) {
-          const float r = __ldcg(reinterpret_cast<const float*>(app.res) + v);
-          act = r > (float)app.eps && atomicExch(app.queued + v, 1u) == 0u;
-        }
+        if (v < app.n) act = app.rs.peek((uint32_t)v) > (double)app.eps && atomicExch(app.queued + v, 1u) == 0u;
         found += q_warp_push(q, act, (uint32_t)v);
       }
       bool done = false;
@@ -240,17 +287,17 @@ __device__ __forceinline__ uint32_t window_sweep(const App& app, const Queue& q,
   uint32_t pushed = 0;
   constexpr int G = 8;
   for (uint32_t i = 0; i < span; i += 32 * G) {
-    float r[G];
+    double r[G];
     uint32_t v[G];
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const uint32_t j = i + lane_id() + 32 * k;
       v[k] = (uint32_t)((s + j) % (uint64_t)app.n);
-      r[k] = j < span ? __ldcg(reinterpret_cast<const float*>(app.res) + v[k]) : 0.f;
+      r[k] = j < span ? app.rs.peek(v[k]) : 0.0;
     }
     bool act[G];
 #pragma unroll
-    for (int k = 0; k < G; ++k) act[k] = r[k] > (float)app.eps && atomicExch(app.queued + v[k], 1u) == 0u;
+    for (int k = 0; k < G; ++k) act[k] = r[k] > (double)app.eps && atomicExch(app.queued + v[k], 1u) == 0u;
     pushed += q_warp_push_multi<G>(q, act, v);
   }
   if (pushed && lane_id() == 0)

@@ -122,13 +122,23 @@ __device__ __forceinline__ uint64_t pol_evict_last() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Column entries carry a HUB TAG in bit 31 (vertex ids are < 2^31 - 1, R10):
+// set at graph create when the target's in-degree is >= HUB_IN_DEG, so the
+// PageRank edge push knows without any extra load that the target keeps its
+// residue in fp64 (R34).  Every reader masks it off with VID_MASK.
+constexpr uint32_t HUB_TAG = 0x80000000u;
+constexpr uint32_t VID_MASK = 0x7FFFFFFFu;
+#ifndef ATOS_HUB_IN_DEG
+#define ATOS_HUB_IN_DEG 512
+#endif
+constexpr uint32_t HUB_IN_DEG = ATOS_HUB_IN_DEG;
 // streaming read-only loads of immutable CSR arrays (no L1 allocation, L2 evict-first)
-__device__ __forceinline__ int32_t ld_col_raw(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_first()));
+__device__ __forceinline__ uint32_t ld_col_tagged(const int32_t* p) {  // raw entry: vertex id | HUB_TAG
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_evict_first()));
   return v;
 }
-__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p) { return ld_col_raw(p); }
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p) { return (int32_t)(ld_col_tagged(p) & VID_MASK); }
 __device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
   int4 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
@@ -244,8 +254,8 @@ struct QueueCtl {
   Line64 processed;
   Line64 abort;         // ABORT_* code (u32 in .v)
   Line64 high_water;    // max observed tail - head
-  Line64 chunk_tail;    // hub chunk table: entries allocated
-  Line64 chunk_done;    // hub chunk table: entries consumed
+  Line64 chunk_tail;    // hub chunk tasks pushed
+  Line64 chunk_done;    // hub chunk tasks consumed
   Line64 trace_count;   // timeline records produced
   Line64 stats[4];      // popped, pushed, edges, spare
   Line64 aux[4];        // app-specific counters (e.g. PR check cursor, colours)
@@ -261,8 +271,7 @@ struct Queue {
   uint64_t deadline;    // %globaltimer deadline (ns); 0 = none (armed by q_arm)
   uint64_t timeout_ns;  // 0 = no watchdog
   uint64_t head_floor;  // discrete rounds: every position < head_floor is claimed
-  struct Chunk* chunks; // hub chunk table (persistent CTA edge-map workers); nullptr = no splitting
-  uint64_t chunk_mask;  // table capacity - 1
+  struct Chunk* chunks; // hub chunk table, ring-capacity entries (persistent CTA edge-map workers); nullptr = no splitting
   struct TraceRec* trace;  // optional timeline (atos_trace_rec); nullptr = off
   uint64_t trace_cap;
   uint32_t trace_kind;
@@ -296,15 +305,18 @@ __device__ __forceinline__ void q_trace(const Queue& q, uint32_t items, uint64_t
   }
 }
 
-// A slice [e0, e1) of a hub's adjacency list, queued as its own task
-// (item = CHUNK_BIT | table index).  payload = the app payload computed when
-// the hub was popped (BFS: dist+1, PR: alpha r / deg).
+// A slice [e0, e1) of a hub's adjacency list, queued as its own task (R24;
+// item = CHUNK_BIT | (p & mask), p = the task's ring position).  The entry of
+// the chunk task at ring position p is chunks[p & mask]: the table has the
+// ring's capacity, a producer writes the entry only after the slot is free for
+// its lap (q_wait_free), and the consumer reads the entry before it releases
+// the slot (st.release) — so an entry is live exactly while its slot is, and
+// the table can neither overflow nor be overwritten under a straggler.
 constexpr uint32_t CHUNK_BIT = 0x80000000u;
 constexpr uint32_t DEFER_BIT = 0x40000000u;  // PageRank: a task deferred once (R31); needs n <= 2^30
 struct Chunk {
-  uint64_t payload;
-  int64_t e0, e1;
-  uint64_t v;  // the hub vertex
+  uint64_t range;  // e0 | (e1 - e0) << 48   (m < 2^48, e1 - e0 <= CHUNK_EDGES)
+  uint64_t pv;     // payload bits; 4-byte payloads carry the hub vertex in bits 32..63
 };
 
 __device__ __forceinline__ bool q_aborted(const Queue& q) {
@@ -323,49 +335,60 @@ __device__ __forceinline__ void q_arm(Queue& q) {
   q.deadline = q.timeout_ns ? globaltimer_ns() + q.timeout_ns : 0;
 }
 
-// Publish `item` at queue position p (a3).  Waits only in the wrap-around case
-// for the previous lap's consumer; detects overflow.  Returns false on abort.
-__device__ __forceinline__ bool q_store_slot(const Queue& q, uint64_t p, uint32_t item) {
-  uint64_t* slot = q.ring + (p & q.mask);
+// Wait until ring position p may be written: in the wrap-around case (lap >
+// 0) the previous lap's item must have been consumed.  Detects overflow (more
+// than cap live, unclaimed items).  Returns false on abort.
+__device__ __forceinline__ bool q_wait_free(const Queue& q, uint64_t p) {
   const uint32_t lap = (uint32_t)(p >> q.log2cap);
-  if (lap > 0) {
-    // wait for "empty for lap" (tag 2*lap); previous lap's item must be consumed
-    unsigned ns = 32;
-    for (;;) {
-      uint32_t tag = (uint32_t)(ld_relaxed_u64(slot) >> 32);
-      if (tag == 2u * lap) break;
-      uint64_t h = ld_relaxed_u64(&q.ctl->head.v);
-      if (h < q.head_floor) h = q.head_floor;
-      if (h + q.mask + 1 <= p) {  // more than cap live (unclaimed) items
-        q_raise(q, ABORT_OVERFLOW);
-        return false;
-      }
-      if (q_aborted(q) || q_timed_out(q)) return false;
-      __nanosleep(ns);
-      ns = ns < 1024 ? ns * 2 : ns;
+  if (lap == 0) return true;
+  const uint64_t* slot = q.ring + (p & q.mask);
+  unsigned ns = 32;
+  for (;;) {
+    uint32_t tag = (uint32_t)(ld_relaxed_u64(slot) >> 32);
+    if (tag == 2u * lap) return true;
+    uint64_t h = ld_relaxed_u64(&q.ctl->head.v);
+    if (h < q.head_floor) h = q.head_floor;
+    if (h + q.mask + 1 <= p) {  // more than cap live (unclaimed) items
+      q_raise(q, ABORT_OVERFLOW);
+      return false;
     }
+    if (q_aborted(q) || q_timed_out(q)) return false;
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : ns;
   }
+}
+
+// Store `item` as the full slot word of position p (slot known to be free).
+__device__ __forceinline__ void q_publish(const Queue& q, uint64_t p, uint32_t item) {
   // Relaxed (strong, L2) store: every push predicate is computed from the
   // RETURNED value of the atomic that produced the state its consumer reads
   // (BFS atomicMin, PR atomicAdd, GC atomicExch after __threadfence), so that
   // atomic is performed at L2 — the point of coherence — before this store
   // issues.  A st.release here cost a MEMBAR+ERRBAR per push (19% of BFS
-  // stall samples, profiles/r01_bfs_rmat24_v1).
-  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(slot),
+  // stall samples, profiles/r01_bfs_rmat24_v1).  (Hub chunk entries are plain
+  // stores and are ordered before their slots by a __threadfence in split_hub.)
+  const uint32_t lap = (uint32_t)(p >> q.log2cap);
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(q.ring + (p & q.mask)),
                "l"(((uint64_t)(2u * lap + 1u) << 32) | item), "l"(pol_evict_first())
                : "memory");
+}
+
+// Publish `item` at queue position p (a3).  Waits only in the wrap-around case
+// for the previous lap's consumer; detects overflow.  Returns false on abort.
+__device__ __forceinline__ bool q_store_slot(const Queue& q, uint64_t p, uint32_t item) {
+  if (!q_wait_free(q, p)) return false;
+  q_publish(q, p, item);
   return true;
 }
 
-// Read the item at position p (claimed by this worker) and mark the slot
-// empty for the next lap.  Returns false only on abort/timeout.
-__device__ __forceinline__ bool q_load_slot(const Queue& q, uint64_t p, uint32_t& item) {
-  uint64_t* slot = q.ring + (p & q.mask);
-  const uint32_t lap = (uint32_t)(p >> q.log2cap);
-  const uint32_t want = 2u * lap + 1u;
+// Read the item at position p (claimed by this worker) without releasing the
+// slot.  Returns false only on abort/timeout.
+__device__ __forceinline__ bool q_read_slot(const Queue& q, uint64_t p, uint32_t& item) {
+  const uint64_t* slot = q.ring + (p & q.mask);
+  const uint32_t want = 2u * (uint32_t)(p >> q.log2cap) + 1u;
   // Relaxed (strong, L2) load: everything the consumer then reads about the
-  // item is addressed THROUGH the item (dist[v], res[v], off[v], chunk[i]) and
-  // read from L2, so it cannot be issued before this load returns.  An
+  // item is addressed THROUGH the item (dist[v], res[v], off[v], chunk entry)
+  // and read from L2, so it cannot be issued before this load returns.  An
   // ld.acquire here adds CCTL.IVALL (L1 invalidate) per item, which would also
   // defeat the L1-cached BFS filter probes.
   uint64_t w = ld_relaxed_u64(slot);
@@ -380,9 +403,69 @@ __device__ __forceinline__ bool q_load_slot(const Queue& q, uint64_t p, uint32_t
     }
   }
   item = (uint32_t)w;
-  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(slot), "l"((uint64_t)(2u * lap + 2u) << 32),
-               "l"(pol_evict_first())
+  return true;
+}
+
+// Mark position p's slot empty for the next lap (after its item was read).
+__device__ __forceinline__ void q_release_slot(const Queue& q, uint64_t p) {
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(q.ring + (p & q.mask)),
+               "l"((uint64_t)(2u * (uint32_t)(p >> q.log2cap) + 2u) << 32), "l"(pol_evict_first())
                : "memory");
+}
+// Release with st.release: every load this thread issued before (the hub
+// chunk entry of the slot) is performed before a producer can see the slot
+// free and rewrite the entry.
+__device__ __forceinline__ void q_release_slot_ordered(const Queue& q, uint64_t p) {
+  st_release_u64(q.ring + (p & q.mask), (uint64_t)(2u * (uint32_t)(p >> q.log2cap) + 2u) << 32);
+}
+
+// Read the item at position p (claimed by this worker) and mark the slot
+// empty for the next lap.  Returns false only on abort/timeout.
+__device__ __forceinline__ bool q_load_slot(const Queue& q, uint64_t p, uint32_t& item) {
+  if (!q_read_slot(q, p, item)) return false;
+  q_release_slot(q, p);
+  return true;
+}
+
+constexpr uint32_t EMPTY_ITEM = 0xFFFFFFFFu;  // never a task word (n < 2^31 - 1, R10)
+
+// Read the claimed positions [first, first + n) into stage[] — participant
+// `me` of `parts` takes items me, me + parts, ... — releasing every slot as
+// soon as its item is read.  An unpublished slot never holds up the others:
+// the participant re-scans its items with backoff until all are in, so a
+// producer waiting for one of these slots to be released for its next lap
+// (ring wrap-around) is never waiting on a consumer that waits on it.
+// Returns false on abort (unread entries stay EMPTY_ITEM).
+__device__ __forceinline__ bool q_read_batch(const Queue& q, uint64_t first, uint32_t n, uint32_t* stage, uint32_t me,
+                                             uint32_t parts) {
+  bool pending = false;
+  for (uint32_t i = me; i < n; i += parts) {
+    const uint64_t p = first + i;
+    const uint64_t w = ld_relaxed_u64(q.ring + (p & q.mask));
+    if ((uint32_t)(w >> 32) == 2u * (uint32_t)(p >> q.log2cap) + 1u) {
+      stage[i] = (uint32_t)w;
+      q_release_slot(q, p);
+    } else {
+      stage[i] = EMPTY_ITEM;
+      pending = true;
+    }
+  }
+  for (unsigned ns = 16; pending; ns = ns < 256 ? ns * 2 : ns) {
+    if (q_aborted(q) || q_timed_out(q)) return false;
+    __nanosleep(ns);
+    pending = false;
+    for (uint32_t i = me; i < n; i += parts) {
+      if (stage[i] != EMPTY_ITEM) continue;
+      const uint64_t p = first + i;
+      const uint64_t w = ld_relaxed_u64(q.ring + (p & q.mask));
+      if ((uint32_t)(w >> 32) == 2u * (uint32_t)(p >> q.log2cap) + 1u) {
+        stage[i] = (uint32_t)w;
+        q_release_slot(q, p);
+      } else {
+        pending = true;
+      }
+    }
+  }
   return true;
 }
 

@@ -17,6 +17,8 @@
 // persistent and discrete schedulers (ring queue) and the BSP variant
 // (frontier arrays).
 #pragma once
+#include <type_traits>
+
 #include "device.cuh"
 
 namespace atos {
@@ -56,7 +58,7 @@ struct BfsApp {
   // any atomic (memory-level parallelism).  The probe may hit a stale L1 copy
   // (>= the current value): it only lets through atomics that turn out not to
   // improve, never suppresses one that would.
-  __device__ __forceinline__ Probe probe(uint32_t w) const {
+  __device__ __forceinline__ Probe probe(uint32_t w, uint32_t /*hub tag*/) const {
     if (!filter) return 0xFFFFFFFFu;
     const uint32_t v = ld_probe_u16(near + w);
     return v == 0xFFFFu ? 0xFFFFFFFFu : v;
@@ -103,9 +105,86 @@ struct BfsApp {
     if (x.e1 == x.e0) return false;
     return atomicMin(done + v, x.d) > x.d;
   }
-  __device__ __forceinline__ bool edge(Payload nd, uint32_t w) const {
-    const Probe pr = probe(w);
+  __device__ __forceinline__ bool edge(Payload nd, uint32_t w, uint32_t tag) const {
+    const Probe pr = probe(w, tag);
     return decide(nd, w, pr, issue(nd, w, pr));
+  }
+};
+
+// PageRank residue storage (R34).  Residues are fp32 (4 B per edge push)
+// except at HUB vertices — in-degree >= HUB_IN_DEG, tagged in the CSR at
+// graph create (device.cuh HUB_TAG) — whose residues are fp64 in res64.  A
+// residue that keeps growing while its vertex waits in the queue rounds away
+// the small pushes it receives: k adds onto an fp32 sum lose up to k 2^-24 of
+// the accumulated mass, and identical pushes (a fan-in hub fed by equal-degree
+// chains) round the same way every time — measured 2.3e-4 of max x* on a
+// 40,000-way fan-in (above the 1e-4 gate).  A vertex receives at most about
+// in-degree adds per queue cycle, so below HUB_IN_DEG = 512 the loss is
+// < 512 2^-24 = 3.1e-5 of its rank even if every rounding had the same sign;
+// at hubs fp64 makes it negligible.  RMAT-24: 55 K hubs take 46% of the edge
+// pushes, on L2-resident lines.  (A TwoSum-compensated fp32 add, tried first,
+// cost +40% on RMAT-24; fp64 residues everywhere +10%.)  With R = double
+// (atos_config.pr_residue_fp64, untagged graphs) every residue is fp64.
+__device__ __forceinline__ float atomic_take(float* p) { return atomicExch(p, 0.0f); }
+__device__ __forceinline__ double atomic_take(double* p) {
+  return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long*>(p), 0ull));
+}
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ void red_add_hot(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol_evict_last()));
+}
+__device__ __forceinline__ void red_add_hot(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol_evict_last()));
+}
+__device__ __forceinline__ bool test_bit(const uint32_t* bits, uint32_t v) {
+  return bits && ((ld_nc_u32(bits + (v >> 5)) >> (v & 31)) & 1u);
+}
+
+template <class R>
+struct Residues {
+  R* res;                // fp32 (or fp64 with R = double) residue per vertex
+  double* res64;         // hub residues (R == float on a tagged graph), indexed by vertex id; else nullptr
+  const uint32_t* hub;   // bit v = v is a hub (pops); nullptr when res64 is
+  __device__ __forceinline__ bool is_hub(uint32_t v) const { return res64 && test_bit(hub, v); }
+  // Alg. 4 line 7, r = atomicExch(residue[v], 0), in two phases so the hub
+  // test never delays the common case: take_issue starts the fp32 exchange
+  // and the hub-bitmap load together (a hub's fp32 word is always 0);
+  // take_finish adds the fp64 exchange for hubs only.
+  struct Take {
+    R r;
+    uint32_t word;  // hub bitmap word of v (0 without hubs)
+  };
+  __device__ __forceinline__ Take take_issue(uint32_t v) const {
+    Take t;
+    t.word = res64 && hub ? ld_nc_u32(hub + (v >> 5)) : 0u;
+    t.r = atomic_take(res + v);
+    return t;
+  }
+  __device__ __forceinline__ double take_finish(uint32_t v, const Take& t) const {
+    return ((t.word >> (v & 31)) & 1u) ? atomic_take(res64 + v) + (double)t.r : (double)t.r;
+  }
+  __device__ __forceinline__ double take(uint32_t v) const { return take_finish(v, take_issue(v)); }
+  // residue[w] += c at the storage the column's hub tag names; returns the old value
+  __device__ __forceinline__ double add(uint32_t w, uint32_t tag, R c) const {
+    if (tag && res64) return atom_add_hot(res64 + w, (double)c);
+    return (double)atom_add_hot(res + w, c);
+  }
+  __device__ __forceinline__ void add_noret(uint32_t w, uint32_t tag, R c) const {
+    if (tag && res64) red_add_hot(res64 + w, (double)c);
+    else red_add_hot(res + w, c);
+  }
+  // did the add of c that returned `old` cross eps (old <= eps < old + c, in the add's own precision)?
+  __device__ __forceinline__ bool crossed(uint32_t tag, double old, R c, R eps) const {
+    if (tag && res64) return old <= (double)eps && old + (double)c > (double)eps;
+    return (R)old <= eps && add_rn((R)old, c) > eps;
+  }
+  __device__ __forceinline__ double peek(uint32_t v) const {  // L2 read (sweeps)
+    return is_hub(v) ? __ldcg(res64 + v) : (double)__ldcg(res + v);
+  }
+  // put a taken residue back (deferral); returns the old value
+  __device__ __forceinline__ double put(uint32_t v, double r) const {
+    return is_hub(v) ? atom_add_hot(res64 + v, r) : (double)atom_add_hot(res + v, (R)r);
   }
 };
 
@@ -113,23 +192,12 @@ struct BfsApp {
 // r = atomicExch(res[v], 0); rank[v] += r; c = alpha r / deg(v);
 // per edge: old = atomicAdd(res[w], c); push w iff old <= eps < old + c.
 // rank accumulates in fp64 (a per-pop cost): a hub receives 10^4+ pops.
-// Residues are R = float (default: 4 B per edge push) or double
-// (atos_config.pr_residue_fp64): a vertex whose claimed task waits long (thread
-// workers with a large FETCH) accumulates a residue of O(10) and fp32 then
-// absorbs pushes below its ulp — measured 6.6e-4 of max(x*) on RMAT-16.
-__device__ __forceinline__ float atomic_take(float* p) { return atomicExch(p, 0.0f); }
-__device__ __forceinline__ double atomic_take(double* p) {
-  return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long*>(p), 0ull));
-}
-__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
-
 template <class R>
 struct PrAppT {
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   double* rank;
-  R* res;
+  Residues<R> rs;
   R alpha, eps;
   // Sink deferral (R29): bit w set = deg(w) == 0.  A dangling vertex's task is
   // `rank += exch(res)` with no effect on any other vertex, so its activation
@@ -145,10 +213,12 @@ struct PrAppT {
   uint32_t defer_deg;  // 0 = off
   R defer_res;
   using Payload = R;
-  __device__ __forceinline__ bool activates(R old, R c, uint32_t w) const {
-    if (!(old <= eps && add_rn(old, c) > eps)) return false;
-    return sink == nullptr || !((ld_nc_u32(sink + (w >> 5)) >> (w & 31)) & 1u);
-  }
+  using Probe = uint32_t;  // the column's hub tag
+  using Raw = double;
+  struct Pre {
+    int64_t e0, e1;
+    typename Residues<R>::Take t;
+  };
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
     Pre x = begin_load(v, g);
@@ -156,41 +226,39 @@ struct PrAppT {
     e1 = x.e1;
     return begin_commit(v, x, p);
   }
-  struct Pre {
-    int64_t e0, e1;
-    R r;
-  };
+  // (deferral only inspects the fp32 part: a hub is never deferred)
   __device__ __forceinline__ bool should_defer(const Pre& x) const {
-    return defer_deg && x.e1 - x.e0 >= (int64_t)defer_deg && x.r < defer_res && x.r > R(0);
+    return defer_deg && x.e1 - x.e0 >= (int64_t)defer_deg && x.t.word == 0u && x.t.r < defer_res && x.t.r > R(0);
   }
   // Put the taken residue back.  If it was <= eps just before (nobody re-pushed
   // v since our take), the caller re-queues v; otherwise a copy is queued already.
-  __device__ __forceinline__ bool put_back(uint32_t v, const Pre& x) const {
-    return atom_add_hot(res + v, x.r) <= eps;
-  }
+  __device__ __forceinline__ bool put_back(uint32_t v, const Pre& x) const { return rs.put(v, (double)x.t.r) <= (double)eps; }
   // the residue exchange is issued in the load phase (its result is only used in commit)
   __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
     Pre x;
     x.e0 = ld_nc_s64(g.off + v);
     x.e1 = ld_nc_s64(g.off + v + 1);
-    x.r = atomic_take(res + v);
+    x.t = rs.take_issue(v);
     return x;
   }
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
-    if (x.r == R(0)) return false;
-    red_add_cold(rank + v, (double)x.r);
+    const double r = rs.take_finish(v, x.t);
+    if (r == 0.0) return false;
+    red_add_cold(rank + v, r);
     if (x.e1 == x.e0) return false;
-    p = alpha * x.r / (R)(x.e1 - x.e0);
+    p = std::is_same<R, float>::value && x.t.word == 0u ? alpha * x.t.r / (R)(x.e1 - x.e0)
+                                                         : (R)((double)alpha * r / (double)(x.e1 - x.e0));
     return true;
   }
-  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const { return activates(atom_add_hot(res + w, c), c, w); }
-  using Probe = int;
-  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
-  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
+  __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const { return rs.add(w, tag, c); }
+  __device__ __forceinline__ bool decide(Payload c, uint32_t w, Probe tag, Raw old) const {
+    if (!rs.crossed(tag, old, c, eps)) return false;
+    return !test_bit(sink, w);
+  }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe tag) const { return decide(c, w, tag, issue(c, w, tag)); }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t tag) const { return commit(c, w, tag); }
   __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
-  using Raw = R;
-  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { return atom_add_hot(res + w, c); }
-  __device__ __forceinline__ bool decide(Payload c, uint32_t w, Probe, Raw old) const { return activates(old, c, w); }
 };
 
 // Asynchronous PageRank with the paper's own activation rule (Alg. 4 lines
@@ -206,33 +274,34 @@ template <class R>
 struct PrWindowAppT {
   static constexpr bool kWindow = true;
   double* rank;
-  R* res;
+  Residues<R> rs;
   uint32_t* queued;
   R alpha, eps;
   int64_t n;
   int check_size;
   using Payload = R;
-  using Probe = int;
+  using Probe = uint32_t;
   using Raw = int;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
   struct Pre {
     int64_t e0, e1;
-    R r;
+    typename Residues<R>::Take t;
   };
   __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
     Pre x;
     x.e0 = ld_nc_s64(g.off + v);
     x.e1 = ld_nc_s64(g.off + v + 1);
     atomicExch(queued + v, 0u);  // a later sweep may re-queue v
-    x.r = atomic_take(res + v);
+    x.t = rs.take_issue(v);
     return x;
   }
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
-    if (x.r == R(0)) return false;
-    red_add_cold(rank + v, (double)x.r);
+    const double r = rs.take_finish(v, x.t);
+    if (r == 0.0) return false;
+    red_add_cold(rank + v, r);
     if (x.e1 == x.e0) return false;
-    p = alpha * x.r / (R)(x.e1 - x.e0);
+    p = (R)((double)alpha * r / (double)(x.e1 - x.e0));
     return true;
   }
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1, Payload& p) const {
@@ -241,19 +310,19 @@ struct PrWindowAppT {
     e1 = x.e1;
     return begin_commit(v, x, p);
   }
-  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
-  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const {
-    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(res + w), "f"((float)c),
-                 "l"(pol_evict_last()));
+  __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
+    rs.add_noret(w, tag, c);
     return 0;
   }
   __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe p) const { return decide(c, w, p, issue(c, w, p)); }
-  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const { return commit(c, w, 0); }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t tag) const { return commit(c, w, tag); }
 };
 
 // BSP PageRank push kernel body (Alg. 3 lines 11-16): same push
-// but the frontier is rebuilt by the filter kernel, so nothing is appended.
+// but the frontier is rebuilt by the filter kernel, so nothing is appended
+// and the adds need no returned value.
 template <class R>
 struct PrBspAppT {
   static constexpr bool kWindow = false;
@@ -264,17 +333,17 @@ struct PrBspAppT {
                                         Payload& p) const {
     return base.begin(v, g, e0, e1, p);
   }
-  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
-    atomicAdd(base.res + w, c);
-    return false;
-  }
-  using Probe = int;
-  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
-  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
-  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
+  using Probe = uint32_t;
   using Raw = int;
-  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { edge(c, w); return 0; }
+  __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
+    base.rs.add_noret(w, tag, c);
+    return 0;
+  }
   __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe tag) const { return decide(c, w, tag, issue(c, w, tag)); }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t tag) const { return commit(c, w, tag); }
+  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
 };
 
 // ------------------------------------------------------- sources / sinks ---
@@ -448,10 +517,6 @@ __device__ __forceinline__ P unpack_payload(uint64_t u) {
   return p;
 }
 
-template <class Src>
-__device__ __forceinline__ const Queue* chunk_queue(const Src&) { return nullptr; }
-__device__ __forceinline__ const Queue* chunk_queue(const RingSrc& s) { return s.q.chunks ? &s.q : nullptr; }
-
 // Load-balancing search expansion of a prepared batch: pre[0..n] is the
 // exclusive prefix of the items' degrees, e0/pay their first edge and payload.
 // Warp `wi` of `nw` takes 32*UNROLL consecutive flattened edges per step; each
@@ -482,9 +547,6 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
     lo = __shfl_sync(FULL_MASK, bound, 0);
     hi = __shfl_sync(FULL_MASK, bound, 31) + 1;
   }
-#ifdef ATOS_STEP_PROF
-  const long long sp0 = clock64();
-#endif
   uint32_t w[U];
   int idx[U];
 #pragma unroll
@@ -496,27 +558,19 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
       lo = lbs_find_range(pre, lo, hi, e);
       idx[k] = lo;
       const int so = sofs ? sofs[lo] : -1;  // staged in shared memory by the agent's TMA copy?
-      w[k] = so >= 0 ? (uint32_t)stage[so + (int)(e - pre[lo])]
-                     : (uint32_t)ld_stream_s32(g.col + e0s[lo] + (e - pre[lo]));
+      w[k] = so >= 0 ? (uint32_t)stage[so + (int)(e - pre[lo])] : ld_col_tagged(g.col + e0s[lo] + (e - pre[lo]));
     }
   }
-#ifdef ATOS_STEP_PROF
-  long long sp1;
-  {
-    uint32_t x = 0;
-#pragma unroll
-    for (int k = 0; k < U; ++k) x ^= w[k];
-    asm volatile("{ .reg .u32 t; add.u32 t, %1, 0; mov.u64 %0, %%clock64; }" : "=l"(sp1) : "r"(x));
-  }
-#endif
   // (value-initialised: an uninitialised raw[k] on lanes without an edge made
   // the compiler carry it across steps through local memory — an LDL/STL
   // pair around every atomic)
   typename App::Probe pr[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) {
+    const uint32_t tag = w[k] >> 31;  // HUB_TAG (device.cuh)
+    w[k] &= VID_MASK;
     pr[k] = typename App::Probe{};
-    if (idx[k] >= 0) pr[k] = app.probe(w[k]);
+    if (idx[k] >= 0) pr[k] = app.probe(w[k], tag);
   }
   typename App::Raw raw[U];
   typename App::Payload pk[U];
@@ -529,31 +583,10 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
   bool act[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) act[k] = idx[k] >= 0 && app.decide(pk[k], w[k], pr[k], raw[k]);
-#ifdef ATOS_STEP_PROF
-  long long sp2;
-  {
-    uint32_t x = 0;
-#pragma unroll
-    for (int k = 0; k < U; ++k) x += act[k];
-    asm volatile("{ .reg .u32 t; add.u32 t, %1, 0; mov.u64 %0, %%clock64; }" : "=l"(sp2) : "r"(x));
-  }
-#endif
   uint32_t item[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) item[k] = app.item_of(w[k]);
-#ifdef ATOS_STEP_PROF
-  const uint32_t pushed_ = sink.template warp_push_multi<U>(act, item);
-  const long long sp3 = clock64();
-  if (lane == 0 && sink.q.ctl) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[6].v), (unsigned long long)(sp1 - sp0));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[7].v), (unsigned long long)(sp2 - sp1));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[8].v), (unsigned long long)(sp3 - sp2));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&sink.q.ctl->prof[9].v), 1ull);
-  }
-  return pushed_;
-#else
   return sink.template warp_push_multi<U>(act, item);
-#endif
 }
 
 template <class App, class Sink>
@@ -579,7 +612,7 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
       if (e < total) {
         lo = lbs_find_range(pre, lo, hi, e);
         idx[k] = lo;
-        w[k] = (uint32_t)ld_col_raw(g.col + e0s[lo] + (e - pre[lo]));
+        w[k] = ld_col_tagged(g.col + e0s[lo] + (e - pre[lo]));
       }
     }
   };
@@ -601,8 +634,12 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
     if (eb + stride < total) fetch(eb + stride, wn, idxn);
     typename App::Probe pr[LBS_UNROLL];
 #pragma unroll
-    for (int k = 0; k < LBS_UNROLL; ++k)
-      if (idx[k] >= 0) pr[k] = app.probe(w[k]);
+    for (int k = 0; k < LBS_UNROLL; ++k) {
+      const uint32_t tag = w[k] >> 31;  // HUB_TAG
+      w[k] &= VID_MASK;
+      pr[k] = typename App::Probe{};
+      if (idx[k] >= 0) pr[k] = app.probe(w[k], tag);
+    }
     typename App::Raw raw[LBS_UNROLL];
     typename App::Payload pk[LBS_UNROLL];
 #pragma unroll
@@ -622,49 +659,49 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
 }
 
 // Publish edges [e0 + CHUNK_EDGES, e1) of hub `v` as chunk tasks; returns the
-// new end of the range the caller keeps (its first chunk).
+// new end of the range the caller keeps (its first chunk).  The entry of the
+// task at ring position p is written to chunks[p & mask] once that slot is
+// free for its lap, then all entries are fenced before the slots are
+// published (device.cuh, Chunk).
 template <class Payload>
 __device__ __noinline__ int64_t split_hub(const Queue* cq, uint32_t v, int64_t e0, int64_t e1, Payload p) {
+  const Queue& q = *cq;
   const uint32_t k = (uint32_t)((e1 - e0 - 1) / CHUNK_EDGES);  // chunks beyond the first
-  const unsigned long long base =
-      atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_tail.v), (unsigned long long)k);
-  if (base + k - ld_relaxed_u64(&cq->ctl->chunk_done.v) > cq->chunk_mask + 1) {
-    q_raise(*cq, ABORT_OVERFLOW);
-    return e1;
-  }
-  const uint64_t pb = pack_payload(p);
+  const unsigned long long base = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->tail.v), (unsigned long long)k);
+  red_add_relaxed_s64(&q.ctl->count.v, (int64_t)k);
+  red_add_relaxed_s64(&q.ctl->chunk_tail.v, (int64_t)k);
+  uint64_t pv = pack_payload(p);
+  if (sizeof(Payload) == 4) pv |= (uint64_t)v << 32;
   for (uint32_t j = 0; j < k; ++j) {
-    Chunk* c = cq->chunks + ((base + j) & cq->chunk_mask);
-    c->payload = pb;
-    c->v = v;
-    c->e0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
-    c->e1 = min(e1, e0 + CHUNK_EDGES * (int64_t)(j + 2));
+    const uint64_t pos = base + j;
+    if (!q_wait_free(q, pos)) return e1;  // aborted: the run is over
+    const int64_t c0 = e0 + CHUNK_EDGES * (int64_t)(j + 1);
+    const int64_t c1 = min(e1, c0 + CHUNK_EDGES);
+    Chunk* c = q.chunks + (pos & q.mask);
+    c->range = (uint64_t)c0 | ((uint64_t)(c1 - c0) << 48);
+    c->pv = pv;
   }
   __threadfence();  // chunk entries visible before their tasks
-  q_thread_push(*cq, k, [&](uint32_t j) { return CHUNK_BIT | (uint32_t)((base + j) & cq->chunk_mask); });
+  for (uint32_t j = 0; j < k; ++j) q_publish(q, base + j, CHUNK_BIT | (uint32_t)((base + j) & q.mask));
   return e0 + CHUNK_EDGES;
 }
 
-// Turn a popped queue item into an edge range + payload (a4 -> a5):
-// a chunk task reads its table entry; a vertex runs the app's begin() and, if
-// it is a hub and splitting is on (cq != nullptr), publishes all but its first
-// CHUNK_EDGES edges as chunk tasks.  Returns false if there is nothing to expand.
+// Read the chunk task at ring position `pos` (its slot read, NOT yet
+// released): edge range + payload, and whether it is still current (BFS: the
+// hub has not improved since).  The caller releases the slot afterwards with
+// q_release_slot_ordered.
 template <class App>
-__device__ __forceinline__ bool prepare_item(const App& app, const GraphView& g, const Queue* cq, uint32_t item,
-                                             int64_t& e0, int64_t& e1, typename App::Payload& p) {
+__device__ __forceinline__ bool read_chunk(const App& app, const Queue& q, uint64_t pos, int64_t& e0, int64_t& e1,
+                                           typename App::Payload& p) {
   using Payload = typename App::Payload;
-  if (cq && (item & CHUNK_BIT)) {
-    const Chunk* c = cq->chunks + (item & ~CHUNK_BIT);
-    e0 = ld_cg_s64(&c->e0);  // L2: table entries are rewritten on wrap
-    e1 = ld_cg_s64(&c->e1);
-    p = unpack_payload<Payload>(ld_cg_u64(&c->payload));
-    const bool ok = app.chunk_current((uint32_t)ld_cg_u64(&c->v), p);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&cq->ctl->chunk_done.v), 1ull);
-    return ok;
-  }
-  if (!app.begin(item, g, e0, e1, p)) return false;
-  if (cq && e1 - e0 > SPLIT_DEG) e1 = split_hub(cq, item, e0, e1, p);
-  return true;
+  const Chunk* c = q.chunks + (pos & q.mask);
+  const uint64_t range = ld_cg_u64(&c->range);  // L2: entries are rewritten on wrap
+  const uint64_t pv = ld_cg_u64(&c->pv);
+  e0 = (int64_t)(range & ((1ull << 48) - 1));
+  e1 = e0 + (int64_t)(range >> 48);
+  p = unpack_payload<Payload>(sizeof(Payload) == 4 ? (pv & 0xFFFFFFFFull) : pv);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->chunk_done.v), 1ull);
+  return app.chunk_current((uint32_t)(pv >> 32), p);
 }
 
 // Process batch items [0, n) with the whole CTA.  Every thread must call.
@@ -673,12 +710,11 @@ __device__ __forceinline__ void cta_batch(const App& app, const GraphView& g, co
                                           uint32_t n, CtaSmem<typename App::Payload>& sm, LocalStats& st) {
   using Payload = typename App::Payload;
   const int T = blockDim.x, tid = threadIdx.x;
-  const Queue* cq = chunk_queue(src);
   for (int i = tid; i < (int)n; i += T) {
     uint32_t item = 0;
     int64_t e0 = 0, e1 = 0;
     Payload p{};
-    bool ok = src.get(i, item) && prepare_item(app, g, cq, item, e0, e1, p);
+    bool ok = src.get(i, item) && app.begin(item, g, e0, e1, p);
     sm.e0[i] = e0;
     sm.pre[i] = ok ? e1 - e0 : 0;
     sm.pay[i] = p;
@@ -708,9 +744,10 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
   {
     const int64_t e = e0 + lane;
     const bool v = e < a0;
-    int32_t w = v ? ld_stream_s32(g.col + e) : 0;
-    bool act = v && app.edge(p, (uint32_t)w);
-    pushed += sink.warp_push(act, app.item_of((uint32_t)w));
+    const uint32_t raw = v ? ld_col_tagged(g.col + e) : 0u;
+    const uint32_t w = raw & VID_MASK;
+    bool act = v && app.edge(p, w, raw >> 31);
+    pushed += sink.warp_push(act, app.item_of(w));
   }
   const int64_t a1 = a0 + ((e1 - a0) & ~int64_t(3));
   const int4* body = reinterpret_cast<const int4*>(g.col + a0);
@@ -719,18 +756,19 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
     const int64_t vi = vb + lane;
     const bool v = vi < nv;
     int4 w4 = v ? ld_stream_v4(body + vi) : make_int4(0, 0, 0, 0);
-    const uint32_t w[4] = {(uint32_t)w4.x, (uint32_t)w4.y, (uint32_t)w4.z, (uint32_t)w4.w};
+    const uint32_t raw[4] = {(uint32_t)w4.x, (uint32_t)w4.y, (uint32_t)w4.z, (uint32_t)w4.w};
+    const uint32_t w[4] = {raw[0] & VID_MASK, raw[1] & VID_MASK, raw[2] & VID_MASK, raw[3] & VID_MASK};
     typename App::Probe pr[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (v) pr[k] = app.probe(w[k]);
-    typename App::Raw raw[4];
+      if (v) pr[k] = app.probe(w[k], raw[k] >> 31);
+    typename App::Raw old[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (v) raw[k] = app.issue(p, w[k], pr[k]);
+      if (v) old[k] = app.issue(p, w[k], pr[k]);
     bool act[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) act[k] = v && app.decide(p, w[k], pr[k], raw[k]);
+    for (int k = 0; k < 4; ++k) act[k] = v && app.decide(p, w[k], pr[k], old[k]);
     uint32_t item[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) item[k] = app.item_of(w[k]);
@@ -739,9 +777,10 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
   {
     const int64_t e = a1 + lane;
     const bool v = e < e1;
-    int32_t w = v ? ld_stream_s32(g.col + e) : 0;
-    bool act = v && app.edge(p, (uint32_t)w);
-    pushed += sink.warp_push(act, app.item_of((uint32_t)w));
+    const uint32_t raw = v ? ld_col_tagged(g.col + e) : 0u;
+    const uint32_t w = raw & VID_MASK;
+    bool act = v && app.edge(p, w, raw >> 31);
+    pushed += sink.warp_push(act, app.item_of(w));
   }
   return pushed;
 }
@@ -806,13 +845,14 @@ __device__ __forceinline__ void thread_batch(const App& app, const GraphView& g,
   refill();
   while (__any_sync(FULL_MASK, e < e1)) {
     bool act = false;
-    int32_t w = 0;
+    uint32_t w = 0;
     if (e < e1) {
-      w = ld_stream_s32(g.col + e);
+      const uint32_t raw = ld_col_tagged(g.col + e);
+      w = raw & VID_MASK;
       ++e;
-      act = app.edge(p, (uint32_t)w);
+      act = app.edge(p, w, raw >> 31);
     }
-    pushed += sink.warp_push(act, app.item_of((uint32_t)w));
+    pushed += sink.warp_push(act, app.item_of(w));
     refill();
   }
   st.edges += edges;

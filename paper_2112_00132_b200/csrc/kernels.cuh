@@ -99,25 +99,24 @@ struct GcPolicy {
 
 // Stage claimed ring positions [first, first+n) into shared memory (warp-collective).
 __device__ __forceinline__ void stage_items(const Queue& q, uint64_t first, uint32_t n, uint32_t* stage) {
-  for (uint32_t i = lane_id(); i < n; i += 32) {
-    uint32_t it = 0xFFFFFFFFu;
-    if (!q_load_slot(q, first + i, it)) it = 0xFFFFFFFFu;
-    stage[i] = it;
-  }
+  q_read_batch(q, first, n, stage, lane_id(), 32);
   __syncwarp();
 }
 struct StageSrc {
   const uint32_t* a;
   __device__ __forceinline__ bool get(uint32_t i, uint32_t& item) const {
     item = a[i];
-    return item != 0xFFFFFFFFu;
+    return item != EMPTY_ITEM;
   }
 };
 
 // dynamic shared memory per block for a worker kind
 template <class P>
 __host__ __device__ inline size_t worker_smem_bytes(int W, int F, int T, bool persistent = false, int S = 0) {
-  if (W == W_CTA) return (persistent && P::kWarpSpecialised) ? P::ws_smem(F, S) : P::smem_bytes(F);
+  if (W == W_CTA) {
+    if (persistent && P::kWarpSpecialised) return P::ws_smem(F, S);
+    return persistent ? align16(P::smem_bytes(F)) + (size_t)F * 4 : P::smem_bytes(F);  // + the staged items
+  }
   if (W == W_WARP) return (size_t)(T / 32) * (size_t)F * 4;
   return (size_t)T * (size_t)F * 4;
 }
@@ -148,7 +147,11 @@ __global__ void __launch_bounds__((W == W_CTA && P::kWarpSpecialised) ? CTA_MAX_
       const uint32_t n = s_n;
       const uint64_t first = s_first;
       if (n == 0) break;
-      RingSrc src{q, first};
+      // every claimed slot is read and released before the batch pushes anything (q_read_batch)
+      uint32_t* stage = reinterpret_cast<uint32_t*>(smem + align16(P::smem_bytes(F)));
+      q_read_batch(q, first, n, stage, threadIdx.x, blockDim.x);
+      __syncthreads();
+      StageSrc src{stage};
       const uint64_t e_before = st.edges;
       P::cta(app, g, src, sink, n, smem, F, st);  // ends with __syncthreads
       if (threadIdx.x == 0) {
@@ -383,23 +386,30 @@ struct PrInitAppT {
     p = c0 / (R)(e1 - e0);
     return true;
   }
-  __device__ __forceinline__ bool edge(Payload c, uint32_t w) const {
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t) const {
     atomicAdd(res + w, c);
     return false;
   }
   using Probe = int;
-  __device__ __forceinline__ Probe probe(uint32_t) const { return 0; }
-  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w); }
+  __device__ __forceinline__ Probe probe(uint32_t, uint32_t) const { return 0; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w, 0); }
   __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
   using Raw = int;
   __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { atomicAdd(res + w, c); return 0; }
   __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
 };
 
+__device__ __forceinline__ bool bit_of(const uint32_t* bits, int64_t v) {
+  return bits && ((bits[v >> 5] >> (v & 31)) & 1u);
+}
+
+// Round the fp64 seeding sums (R30) to the residue storage (R34): a hub keeps
+// its sum in fp64 (res64 is the sums array itself) and its fp32 word is 0;
+// every other vertex takes the sum rounded once to R.
 template <class R>
-__global__ void k_f64_to_res(const double* a, R* b, int64_t n) {
+__global__ void k_f64_to_res(const double* a, R* b, const uint32_t* hub, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = (R)a[i];
+    b[i] = bit_of(hub, i) ? R(0) : (R)a[i];
 }
 
 __global__ void k_f64_to_f32(const double* a, float* b, int64_t n) {
@@ -416,16 +426,42 @@ __global__ void k_sink_bitmap(const int64_t* off, int64_t n, uint32_t* bits) {
   }
 }
 
+// Hub tagging (R34), at graph create: in-degree histogram, then bit 31 of
+// every column entry whose target has in-degree >= thr, and the hub bitmap.
+__global__ void k_in_degree(const int32_t* col, int64_t m, uint32_t* indeg) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(indeg + (col[e] & VID_MASK), 1u);
+}
+__global__ void k_tag_hubs(int32_t* col, int64_t m, const uint32_t* indeg, uint32_t thr) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = (uint32_t)col[e] & VID_MASK;
+    col[e] = (int32_t)(w | (indeg[w] >= thr ? HUB_TAG : 0u));
+  }
+}
+__global__ void k_hub_bitmap(const uint32_t* indeg, int64_t n, uint32_t thr, uint32_t* bits,
+                             unsigned long long* count) {
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = b + lane_id();
+    const uint32_t m = __ballot_sync(FULL_MASK, v < n && indeg[v] >= thr);
+    if (lane_id() == 0) {
+      bits[b >> 5] = m;
+      if (m) atomicAdd(count, (unsigned long long)__popc(m));
+    }
+  }
+}
+
 // Sink absorption (R29): after quiescence every dangling vertex performs its
 // deferred task body `rank[v] += exch(res[v], 0)` (Alg. 4 line 8 with deg 0, R5).
 template <class R>
-__global__ void k_pr_absorb_sinks(const uint32_t* __restrict__ bits, R* res, double* rank, int64_t n) {
+__global__ void k_pr_absorb_sinks(const uint32_t* __restrict__ bits, Residues<R> rs, double* rank, int64_t n) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     if ((bits[v >> 5] >> (v & 31)) & 1u) {
-      const R r = res[v];
-      if (r != R(0)) {
-        rank[v] += (double)r;
-        res[v] = R(0);
+      const bool h = rs.res64 && bit_of(rs.hub, v);
+      const double r = h ? rs.res64[v] : (double)rs.res[v];
+      if (r != 0.0) {
+        rank[v] += r;
+        if (h) rs.res64[v] = 0.0;
+        else rs.res[v] = R(0);
       }
     }
   }
@@ -433,23 +469,27 @@ __global__ void k_pr_absorb_sinks(const uint32_t* __restrict__ bits, R* res, dou
 
 // BSP PageRank filter kernel (Alg. 3 lines 18-22): residue > eps -> frontier
 template <class R>
-__global__ void k_pr_filter(const R* res, int64_t n, R eps, uint32_t* out, unsigned long long* count) {
+__global__ void k_pr_filter(Residues<R> rs, int64_t n, R eps, uint32_t* out, unsigned long long* count) {
   ArraySink sink{out, count};
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; b < n; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = b + lane_id();
-    const bool a = v < n && res[v] > eps;
+    bool a = false;
+    if (v < n) a = (rs.res64 && bit_of(rs.hub, v)) ? rs.res64[v] > (double)eps : rs.res[v] > eps;
     sink.warp_push(a, (uint32_t)v);
   }
 }
 
-// max reduction helpers for stats
+// max over v of the residue (stats.max_residue), as float bits
 template <class R>
-__global__ void k_max_f32(const R* a, int64_t n, unsigned int* out_bits) {
+__global__ void k_max_res(Residues<R> rs, int64_t n, unsigned int* out_bits) {
   float m = 0.f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) m = fmaxf(m, (float)a[i]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, (rs.res64 && bit_of(rs.hub, i)) ? (float)rs.res64[i] : (float)rs.res[i]);
   for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL_MASK, m, d));
   if (lane_id() == 0) atomicMax(out_bits, __float_as_uint(m));  // m >= 0 so bit order == value order
 }
+
+// max reduction helpers for stats
 __global__ void k_max_s32(const int32_t* a, int64_t n, int* out) {
   int m = -1;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) m = max(m, a[i]);

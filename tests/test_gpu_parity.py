@@ -166,8 +166,9 @@ def test_bfs_deep_path_beyond_u16_mirror(atos):
 
 def test_trace_records(atos):
     g = G("rmat16")
-    tr = atos.Trace(1 << 16)
+    tr = atos.Trace(1 << 22)
     d, st = atos.bfs(D(atos, "rmat16"), 0, trace=tr)
+    assert np.array_equal(d, oracle.bfs(g, 0))  # tracing writes from the hot loop: results must not change
     r = tr.records(st)
     assert st["trace_records"] == len(r) > 0
     assert np.all(np.diff(r["t_ns"].astype(np.int64)) >= 0)
@@ -175,6 +176,16 @@ def test_trace_records(atos):
     assert int(r["items"].sum()) == st["tasks_popped"] + st["chunk_tasks"]
     assert int(r["edges"].astype(np.int64).sum()) == st["edges_processed"]
     assert set(np.unique(r["kind"]).tolist()) == {0}
+    # PageRank and colouring with the timeline on: parity and record accounting
+    x = jacobi("rmat16")
+    rk, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, trace=tr)
+    assert np.max(np.abs(rk.astype(np.float64) - x)) / x.max() <= PR_TOL and st["max_residue"] <= 1e-6
+    r = tr.records(st)
+    assert int(r["items"].sum()) == st["tasks_popped"] + st["chunk_tasks"] and set(np.unique(r["kind"]).tolist()) == {1}
+    c, k, st = atos.color(D(atos, "rmat16s", symmetric=True), trace=tr)
+    assert oracle.check_coloring(G("rmat16s"), c)[0] == 0
+    r = tr.records(st)
+    assert int(r["items"].sum()) == st["tasks_popped"] and set(np.unique(r["kind"]).tolist()) == {2}
 
 
 def test_stats_invariants(atos):
@@ -199,7 +210,7 @@ def test_discrete_device_loop(atos, worker):
         assert st["rounds"] == st2["rounds"], name  # same rounds as the host-driven loop
     x = jacobi("rmat16")
     r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel="discrete", device_loop=True, worker=worker,
-                          fetch_size=32, pr_residue_fp64=worker == "thread")
+                          fetch_size=32)
     assert np.max(np.abs(r - x)) / x.max() <= PR_TOL and st["max_residue"] <= 1e-6
     c, k, st = atos.color(D(atos, "rmat16s", symmetric=True), kernel="discrete", device_loop=True, worker=worker)
     assert oracle.check_coloring(G("rmat16s"), c)[0] == 0
@@ -270,6 +281,46 @@ def test_bfs_queue_wraparound(atos):
     assert st["tasks_pushed"] > 256  # wrapped the ring
 
 
+def hub_chain(k=300, deg=5000):
+    """k hubs in a chain: hub i has `deg` parallel edges to hub i+1, so every hub is
+    split into chunk tasks (R24) while the frontier stays one vertex wide."""
+    off = np.arange(k + 2, dtype=np.int64) * deg
+    off[-1] = off[-2]  # the last vertex has no edges
+    col = np.repeat(np.arange(1, k + 1, dtype=np.int32), deg)
+    return off, col
+
+
+@pytest.mark.parametrize("gname,cap", [("grid64", 256), ("road", 256), ("hubchain", 256)])
+@pytest.mark.parametrize("fetch,threads", [(128, 256), (16, 64), (512, 1024)])
+def test_bfs_cta_queue_wraparound(atos, gname, cap, fetch, threads):
+    """Persistent CTA workers (queue agent, hub chunk tasks) on a small ring:
+    the agent reads every claimed slot before it pushes, chunk
+    entries live exactly as long as their slots; exact depths, no hang."""
+    if gname == "hubchain":
+        off, col = hub_chain()
+        Gd = atos.Graph(off, col)
+        exp = np.arange(301, dtype=np.uint32)
+    else:
+        Gd, exp = D(atos, gname), oracle.bfs(G(gname), 0)
+    d, st = atos.bfs(Gd, 0, queue_capacity=cap, fetch_size=fetch, cta_threads=threads, timeout_s=60)
+    assert np.array_equal(d, exp)
+    assert st["tasks_pushed"] + st["chunk_tasks"] > cap  # wrapped the ring
+    if gname == "hubchain":
+        assert st["chunk_tasks"] >= 300
+
+
+@pytest.mark.parametrize("worker", WORKERS)
+def test_pagerank_queue_wraparound(atos, worker):
+    """PageRank on a 2n-slot ring (threshold activation keeps <= 2 live copies
+    per vertex, R16): the pushes wrap the ring several times."""
+    g = G("rmat12")
+    x = jacobi("rmat12")
+    r, st = atos.pagerank(D(atos, "rmat12"), 0.85, 1e-6, worker=worker, fetch_size=32, queue_capacity=2 * g.n,
+                          timeout_s=60)
+    assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
+    assert st["tasks_pushed"] > 4 * g.n
+
+
 def test_bfs_queue_overflow(atos):
     with pytest.raises(atos.AtosError) as e:
         atos.bfs(D(atos, "star"), 0, queue_capacity=32, num_blocks=1)
@@ -320,18 +371,16 @@ def jacobi(name, alpha=0.85):
 @pytest.mark.parametrize("kernel,worker,fetch", [(k, w, f) for k in KERNELS for w in WORKERS for f in (1, 32, 256)])
 def test_pagerank_matrix(atos, kernel, worker, fetch):
     x = jacobi("rmat16")
-    # Thread workers with a large FETCH hold claimed vertices long enough for
-    # their pending residue to grow to O(10); fp32 then absorbs pushes below
-    # its ulp (measured 6.6e-4 of max x* at FETCH 256), so those cells run with
-    # fp64 residues (atos_config.pr_residue_fp64).
-    r64 = worker == "thread" and fetch >= 32
+    # fp32 residues in every cell: thread workers with a large FETCH hold claimed
+    # vertices long enough for their residue to grow to O(10), which rounded
+    # away 6.6e-4 of max x* before the compensated adds (DESIGN R34)
     r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=fetch,
-                          cta_threads=T(worker, fetch), pr_residue_fp64=r64)
+                          cta_threads=T(worker, fetch))
     err = np.max(np.abs(r.astype(np.float64) - x)) / x.max()
     assert err <= PR_TOL, err
     assert st["max_residue"] <= 1e-6
-    # one-sided bound 0 <= x* - rank <= eps x*/(1-a) (+ fp32 rounding)
-    assert np.all(r <= x * (1 + 1e-5) + 2e-5 * x.max())  # fp32 rounding may overshoot slightly
+    # one-sided bound 0 <= x* - rank <= eps x*/(1-a) (Alg. 4 invariant; R34 keeps it through fp32)
+    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
 
 
 @pytest.mark.parametrize("worker", WORKERS)
@@ -357,10 +406,10 @@ def test_pagerank_sink_defer(atos, kernel, worker):
     pushed = {}
     for defer in (False, True):
         r, st = atos.pagerank(D(atos, "rmat16"), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
-                              cta_threads=T(worker, 32), pr_residue_fp64=worker == "thread", sink_defer=defer)
+                              cta_threads=T(worker, 32), sink_defer=defer)
         assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
         assert st["max_residue"] <= 1e-6
-        assert np.all(r <= x * (1 + 1e-5) + 2e-5 * x.max())  # fp32 rounding may overshoot slightly
+        assert np.all(r <= x * (1 + 1e-5) + 1e-6)
         pushed[defer] = st["tasks_pushed"]
     assert pushed[True] < pushed[False], pushed
 
@@ -385,52 +434,64 @@ def test_pagerank_hub_deferral(atos, gname, deg, factor):
     x = oracle.pagerank(g, 0.85)[0]
     Gd = atos.Graph.from_csr(g) if gname == "fanin" else D(atos, gname)
     # deferring the fan-in hub lets its fp32 residue grow for a second queue cycle while
-    # eps-sized pushes arrive, which then round away (1.1e-4 / 1.8e-4 of max x* measured
-    # with fp32 residues at (1, 1000) / (16, 4)): that graph runs with fp64 residues (R31)
-    r, st = atos.pagerank(Gd, 0.85, 1e-6, fetch_size=64, pr_defer_degree=deg, pr_defer_factor=factor,
-                          pr_residue_fp64=gname == "fanin")
+    # eps-sized pushes arrive (1.1e-4 / 1.8e-4 of max x* rounded away before R34)
+    r, st = atos.pagerank(Gd, 0.85, 1e-6, fetch_size=64, pr_defer_degree=deg, pr_defer_factor=factor)
     assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
     assert st["max_residue"] <= 1e-6
-    assert np.all(r <= x * (1 + 1e-5) + 2e-5 * x.max())  # fp32 rounding may overshoot slightly
+    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
 
 
 def fan_in_graph(k=40000, fan=64):
     """k sources s -> 0 and s -> s+1 (chain), plus 0 -> 1..fan: vertex 0's
     seeding residue (R4) is k adds of the same c = (1-a)a/2 onto a sum growing
     to ~2,550, whose fp32 rounding errors are correlated (R30)."""
-    edges = [(s, 0) for s in range(1, k + 1)] + [(s, s + 1) for s in range(1, k)] + [(0, j) for j in range(1, fan + 1)]
-    return gg.from_edges(k + 1, edges, name="fanin")
+    if "graph" not in _fan:
+        edges = [(s, 0) for s in range(1, k + 1)] + [(s, s + 1) for s in range(1, k)] + [(0, j) for j in range(1, fan + 1)]
+        _fan["graph"] = gg.from_edges(k + 1, edges, name="fanin")
+    return _fan["graph"]
 
 
-@pytest.mark.parametrize("kernel", ["persistent", "discrete"])
+@pytest.mark.parametrize("r64", [False, True])
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("worker", WORKERS)
-def test_pagerank_fan_in_hub(atos, kernel, worker):
-    """A 40,000-way fan-in hub (x* = 11,930) with fp64 residues: the seeding
-    (fp64 sums, R30) and the main phase reach the Jacobi fixed point.  With
-    fp32 residues this graph loses eps-sized pushes at the hub (1.8e-4 to
-    5.8e-4 of max x* measured, every worker; R32) — see the one-sided test."""
+def test_pagerank_fan_in_hub(atos, kernel, worker, r64):
+    """A 40,000-way fan-in hub (x* = 11,930) fed by 40,000 equal pushes per
+    sweep: fp32 residues rounded them the same way every time (1.8e-4 to
+    5.8e-4 of max x* before the compensated adds, DESIGN R32/R34).  Both
+    residue precisions must meet the gate and the one-sided bound."""
     g = fan_in_graph()
-    x = oracle.pagerank(g, 0.85)[0]
-    r, st = atos.pagerank(atos.Graph.from_csr(g), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
-                          cta_threads=T(worker, 32), pr_residue_fp64=True)
+    x = fan_in_x()
+    r, st = atos.pagerank(fan_in_dev(atos), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
+                          cta_threads=T(worker, 32), pr_residue_fp64=r64)
     err = np.max(np.abs(r.astype(np.float64) - x)) / x.max()
     assert err <= PR_TOL, err
     assert st["max_residue"] <= 1e-6
+    assert np.all(r <= x * (1 + 1e-5) + 1e-6)
 
 
-@pytest.mark.parametrize("kernel", ["persistent", "discrete"])
+_fan = {}
+
+
+def fan_in_x():
+    if "x" not in _fan:
+        _fan["x"] = oracle.pagerank(fan_in_graph(), 0.85)[0]
+    return _fan["x"]
+
+
+def fan_in_dev(atos):
+    if "g" not in _fan:
+        _fan["g"] = atos.Graph.from_csr(fan_in_graph())
+    return _fan["g"]
+
+
+@pytest.mark.parametrize("fetch", [1, 32, 256, 1024])
 @pytest.mark.parametrize("worker", WORKERS)
-def test_pagerank_fp32_fan_in_error_bounded(atos, kernel, worker):
-    """Characterises the documented fp32-residue limit (DESIGN R32) on the
-    fan-in hub: measured 1.8e-4 to 5.8e-4 of max x* (rounding of eps-sized
-    adds onto a large residue, either sign); it must stay far below the
-    answer's scale.  Acceptance-grade runs on such graphs use fp64 residues
-    (test_pagerank_fan_in_hub)."""
-    g = fan_in_graph()
-    x = oracle.pagerank(g, 0.85)[0]
-    r, st = atos.pagerank(atos.Graph.from_csr(g), 0.85, 1e-6, kernel=kernel, worker=worker, fetch_size=32,
-                          cta_threads=T(worker, 32))
-    assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= 2e-3
+def test_pagerank_fan_in_fetch_sweep(atos, worker, fetch):
+    """Large FETCH holds claimed vertices (and their growing residues) longest."""
+    x = fan_in_x()
+    r, st = atos.pagerank(fan_in_dev(atos), 0.85, 1e-6, worker=worker, fetch_size=fetch,
+                          cta_threads=T(worker, fetch))
+    assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
     assert st["max_residue"] <= 1e-6
 
 
