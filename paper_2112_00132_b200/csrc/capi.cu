@@ -180,6 +180,8 @@ extern "C" void atos_config_default(atos_config* c) {
   c->hub_split = -1;
 }
 
+static atos_status check_failures();
+
 static atos_status check_config(const atos_config* c) {
   if (c->struct_size != sizeof(atos_config))
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "atos_config.struct_size %u != %zu (use atos_config_default)",
@@ -303,7 +305,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     uint32_t* indeg = nullptr;
     CK(pool_malloc(&indeg, (size_t)n * sizeof(uint32_t)));
     CK(cudaMemset(indeg, 0, (size_t)n * sizeof(uint32_t)));
-    k_in_degree<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, indeg);
+    k_in_degree<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, indeg);
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g->d_scratch) + 4;
     CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
     CK(pool_malloc(&g->d_hub, (size_t)((n + 31) / 32) * sizeof(uint32_t)));
@@ -311,14 +313,14 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     unsigned long long hubs = 0;
     CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
     g->num_hubs = (int64_t)hubs;
-    if (hubs) k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, indeg, HUB_IN_DEG);
+    if (hubs) k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, indeg, HUB_IN_DEG);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     pool_free(indeg);
   }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
-  return ATOS_OK;
+  return check_failures();
 }
 
 static void graph_free(atos_graph g) {
@@ -447,6 +449,29 @@ static Queue make_queue(atos_graph g, const atos_config& cfg, uint32_t kind) {
   return q;
 }
 
+// Checked builds (-DATOS_CHECKED, device.cuh chk): report and clear the first
+// failed bounds check of the last kernels.  Product builds: always OK.
+static atos_status check_failures() {
+#ifdef ATOS_CHECKED
+  {
+    CheckRec r{};
+    CK(cudaMemcpyFromSymbol(&r, g_atos_check, sizeof r));
+    if (r.hit) {
+      const CheckRec z{};
+      CK(cudaMemcpyToSymbol(g_atos_check, &z, sizeof z));
+      const char* names[] = {"engine.cuh", "gc.cuh", "cta_ws.cuh", "cta_ws2.cuh", "kernels.cuh", "dist_impl.cuh",
+                             "device.cuh"};
+      const char* f = "?";
+      for (const char* nm : names)
+        if (chk_fhash(nm) == r.file) f = nm;
+      return atos_set_error(ATOS_ERR_CUDA, "bounds check failed at %s:%u (index %lld, bound %lld)", f, r.line,
+                            r.value, r.bound);
+    }
+  }
+#endif
+  return ATOS_OK;
+}
+
 // Read back the control block; translate abort codes.
 static atos_status read_ctl(atos_graph g, cudaStream_t s) {
   CK(cudaMemcpyAsync(g->ws.h_ctl, g->ws.ctl, sizeof(QueueCtl), cudaMemcpyDeviceToHost, s));
@@ -457,7 +482,7 @@ static atos_status read_ctl(atos_graph g, cudaStream_t s) {
                           "queue_capacity", (unsigned long long)g->ws.cap);
   if (ab == ABORT_TIMEOUT) return atos_set_error(ATOS_ERR_TIMEOUT, "device watchdog fired");
   if (ab) return atos_set_error(ATOS_ERR_CUDA, "unknown abort code %llu", (unsigned long long)ab);
-  return ATOS_OK;
+  return check_failures();
 }
 
 // ------------------------------------------------------------------ launchers

@@ -233,6 +233,44 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// ---- bounds-checked builds (-DATOS_CHECKED; tests/test_queue_stress.py).  Every
+// index the hot path derives from device data (a popped task word, a CSR offset,
+// a column entry, a shared-memory batch offset) passes through chk(): in a
+// checked build an out-of-range index records (file hash, line, value) in
+// g_atos_check — the first failure wins — and is clamped to 0 so the access
+// stays in bounds; the call then returns ATOS_ERR_CUDA naming the check.  In
+// product builds chk() is the identity.  (compute-sanitizer is not available
+// on this pool, so this is the out-of-bounds detector.)
+__host__ __device__ constexpr uint32_t chk_fnv(const char* s, uint32_t h = 2166136261u) {
+  return *s ? chk_fnv(s + 1, (h ^ (uint32_t)(unsigned char)*s) * 16777619u) : h;
+}
+__host__ __device__ constexpr const char* chk_base(const char* s, const char* b = nullptr) {
+  return *s ? chk_base(s + 1, *s == '/' ? s + 1 : (b ? b : s)) : (b ? b : s);
+}
+__host__ __device__ constexpr uint32_t chk_fhash(const char* path) { return chk_fnv(chk_base(path)); }
+struct CheckRec {
+  unsigned long long hit;  // 0 = clean
+  uint32_t file, line;
+  long long value, bound;
+};
+#ifdef ATOS_CHECKED
+__device__ CheckRec g_atos_check;
+__device__ __noinline__ void chk_fail(uint32_t file, uint32_t line, long long v, long long bound) {
+  if (atomicCAS(&g_atos_check.hit, 0ull, 1ull) == 0ull) {
+    g_atos_check.file = file;
+    g_atos_check.line = line;
+    g_atos_check.value = v;
+    g_atos_check.bound = bound;
+    __threadfence();
+  }
+}
+#define ATOS_CHK(i, bound) \
+  (((unsigned long long)(long long)(i) < (unsigned long long)(long long)(bound)) ? (i) \
+   : (::atos::chk_fail(::atos::chk_fhash(__FILE__), __LINE__, (long long)(i), (long long)(bound)), decltype(i)(0)))
+#else
+#define ATOS_CHK(i, bound) (i)
+#endif
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

@@ -94,6 +94,7 @@ struct BfsApp {
     uint32_t d;
   };
   __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
+    v = ATOS_CHK(v, (uint32_t)g.n);  // a popped task word
     Pre x;
     x.e0 = ld_nc_s64(g.off + v);
     x.e1 = ld_nc_s64(g.off + v + 1);
@@ -235,6 +236,7 @@ struct PrAppT {
   __device__ __forceinline__ bool put_back(uint32_t v, const Pre& x) const { return rs.put(v, (double)x.t.r) <= (double)eps; }
   // the residue exchange is issued in the load phase (its result is only used in commit)
   __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
+    v = ATOS_CHK(v, (uint32_t)g.n);  // a popped task word
     Pre x;
     x.e0 = ld_nc_s64(g.off + v);
     x.e1 = ld_nc_s64(g.off + v + 1);
@@ -289,6 +291,7 @@ struct PrWindowAppT {
     typename Residues<R>::Take t;
   };
   __device__ __forceinline__ Pre begin_load(uint32_t v, const GraphView& g) const {
+    v = ATOS_CHK(v, (uint32_t)g.n);  // a popped task word
     Pre x;
     x.e0 = ld_nc_s64(g.off + v);
     x.e1 = ld_nc_s64(g.off + v + 1);
@@ -555,10 +558,11 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
     idx[k] = -1;
     w[k] = 0;
     if (e < total) {
-      lo = lbs_find_range(pre, lo, hi, e);
+      lo = ATOS_CHK(lbs_find_range(pre, lo, hi, e), n);
       idx[k] = lo;
       const int so = sofs ? sofs[lo] : -1;  // staged in shared memory by the agent's TMA copy?
-      w[k] = so >= 0 ? (uint32_t)stage[so + (int)(e - pre[lo])] : ld_col_tagged(g.col + e0s[lo] + (e - pre[lo]));
+      w[k] = so >= 0 ? (uint32_t)stage[so + (int)(e - pre[lo])]
+                     : ld_col_tagged(g.col + ATOS_CHK(e0s[lo] + (e - pre[lo]), g.col_cap));
     }
   }
   // (value-initialised: an uninitialised raw[k] on lanes without an edge made
@@ -568,7 +572,7 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
 #pragma unroll
   for (int k = 0; k < U; ++k) {
     const uint32_t tag = w[k] >> 31;  // HUB_TAG (device.cuh)
-    w[k] &= VID_MASK;
+    w[k] = ATOS_CHK(w[k] & VID_MASK, g.n);
     pr[k] = typename App::Probe{};
     if (idx[k] >= 0) pr[k] = app.probe(w[k], tag);
   }
@@ -610,9 +614,9 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
       idx[k] = -1;
       w[k] = 0;
       if (e < total) {
-        lo = lbs_find_range(pre, lo, hi, e);
+        lo = ATOS_CHK(lbs_find_range(pre, lo, hi, e), n);
         idx[k] = lo;
-        w[k] = ld_col_tagged(g.col + e0s[lo] + (e - pre[lo]));
+        w[k] = ld_col_tagged(g.col + ATOS_CHK(e0s[lo] + (e - pre[lo]), g.col_cap));
       }
     }
   };
@@ -636,7 +640,7 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k) {
       const uint32_t tag = w[k] >> 31;  // HUB_TAG
-      w[k] &= VID_MASK;
+      w[k] = ATOS_CHK(w[k] & VID_MASK, g.n);
       pr[k] = typename App::Probe{};
       if (idx[k] >= 0) pr[k] = app.probe(w[k], tag);
     }
@@ -744,8 +748,8 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
   {
     const int64_t e = e0 + lane;
     const bool v = e < a0;
-    const uint32_t raw = v ? ld_col_tagged(g.col + e) : 0u;
-    const uint32_t w = raw & VID_MASK;
+    const uint32_t raw = v ? ld_col_tagged(g.col + ATOS_CHK(e, g.col_cap)) : 0u;
+    const uint32_t w = ATOS_CHK(raw & VID_MASK, g.n);
     bool act = v && app.edge(p, w, raw >> 31);
     pushed += sink.warp_push(act, app.item_of(w));
   }
@@ -755,9 +759,10 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
   for (int64_t vb = 0; vb < nv; vb += 32) {
     const int64_t vi = vb + lane;
     const bool v = vi < nv;
-    int4 w4 = v ? ld_stream_v4(body + vi) : make_int4(0, 0, 0, 0);
+    int4 w4 = v ? ld_stream_v4(body + ATOS_CHK(vi, (g.col_cap - a0) >> 2)) : make_int4(0, 0, 0, 0);
     const uint32_t raw[4] = {(uint32_t)w4.x, (uint32_t)w4.y, (uint32_t)w4.z, (uint32_t)w4.w};
-    const uint32_t w[4] = {raw[0] & VID_MASK, raw[1] & VID_MASK, raw[2] & VID_MASK, raw[3] & VID_MASK};
+    const uint32_t w[4] = {ATOS_CHK(raw[0] & VID_MASK, g.n), ATOS_CHK(raw[1] & VID_MASK, g.n),
+                           ATOS_CHK(raw[2] & VID_MASK, g.n), ATOS_CHK(raw[3] & VID_MASK, g.n)};
     typename App::Probe pr[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -777,8 +782,8 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
   {
     const int64_t e = a1 + lane;
     const bool v = e < e1;
-    const uint32_t raw = v ? ld_col_tagged(g.col + e) : 0u;
-    const uint32_t w = raw & VID_MASK;
+    const uint32_t raw = v ? ld_col_tagged(g.col + ATOS_CHK(e, g.col_cap)) : 0u;
+    const uint32_t w = ATOS_CHK(raw & VID_MASK, g.n);
     bool act = v && app.edge(p, w, raw >> 31);
     pushed += sink.warp_push(act, app.item_of(w));
   }
@@ -847,8 +852,8 @@ __device__ __forceinline__ void thread_batch(const App& app, const GraphView& g,
     bool act = false;
     uint32_t w = 0;
     if (e < e1) {
-      const uint32_t raw = ld_col_tagged(g.col + e);
-      w = raw & VID_MASK;
+      const uint32_t raw = ld_col_tagged(g.col + ATOS_CHK(e, g.col_cap));
+      w = ATOS_CHK(raw & VID_MASK, g.n);
       ++e;
       act = app.edge(p, w, raw >> 31);
     }

@@ -95,7 +95,7 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
     sm.flag[i] = 0;
     if (t != 0xFFFFFFFFu) {
       const uint32_t v = t & ~GC_CHECK_BIT;
-      sm.e0[i] = ld_nc_s64(g.off + v);
+      sm.e0[i] = ld_nc_s64(g.off + ATOS_CHK(v, g.n));
       sm.pre[i] = ld_nc_s64(g.off + v + 1) - sm.e0[i];
       if (t & GC_CHECK_BIT) {
         sm.col_v[i] = ld_relaxed_s32(app.color + app.vb + v);
@@ -127,7 +127,7 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
         const int i = lbs_find(sm.pre, (int)n, e);
         const uint32_t t = sm.task[i];
         const uint32_t v = (t & ~GC_CHECK_BIT) + app.vb;  // global id
-        const uint32_t u = (uint32_t)ld_stream_s32(g.col + sm.e0[i] + (e - sm.pre[i]));
+        const uint32_t u = (uint32_t)ld_stream_s32(g.col + ATOS_CHK(sm.e0[i] + (e - sm.pre[i]), g.col_cap));
         if (u != v) {
           const int32_t cu = ld_relaxed_s32(app.color + u);
           if (t & GC_CHECK_BIT) {
@@ -222,7 +222,7 @@ __device__ __forceinline__ uint32_t gc_warp_task(const GcApp& app, const GraphVi
   const int lane = lane_id();
   const uint32_t v = t & ~GC_CHECK_BIT;  // local id
   const uint32_t vg = v + app.vb;        // global id
-  const int64_t e0 = ld_nc_s64(g.off + v), e1 = ld_nc_s64(g.off + v + 1);
+  const int64_t e0 = ld_nc_s64(g.off + ATOS_CHK(v, g.n)), e1 = ld_nc_s64(g.off + v + 1);
   uint32_t pushed = 0;
   if (t & GC_CHECK_BIT) {
     const int32_t c = ld_relaxed_s32(app.color + vg);
@@ -233,7 +233,7 @@ __device__ __forceinline__ uint32_t gc_warp_task(const GcApp& app, const GraphVi
       bool act = false;
       uint32_t u = 0;
       if (e < e1) {
-        u = (uint32_t)ld_stream_s32(g.col + e);
+        u = (uint32_t)ld_stream_s32(g.col + ATOS_CHK(e, g.col_cap));
         if (u != vg && ld_relaxed_s32(app.color + u) == c) {
           if (u < vg) self = true;
           else if (MODE == GC_UBER && app.owned(u)) {
@@ -271,7 +271,7 @@ __device__ __forceinline__ uint32_t gc_warp_task(const GcApp& app, const GraphVi
     for (int k = 0; k < GC_WIN_WORDS; ++k) m[k] = 0;
     edges += e1 - e0;
     for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const uint32_t u = (uint32_t)ld_stream_s32(g.col + e);
+      const uint32_t u = (uint32_t)ld_stream_s32(g.col + ATOS_CHK(e, g.col_cap));
       if (u == vg) continue;
       const int32_t r = ld_relaxed_s32(app.color + u) - base;
       if (r >= 0 && r < 32 * GC_WIN_WORDS) {
@@ -305,7 +305,7 @@ __device__ __forceinline__ uint32_t gc_thread_task(const GcApp& app, const Graph
   const uint32_t v = t & ~GC_CHECK_BIT;  // local id
   const uint32_t vg = v + app.vb;        // global id
   int64_t e0 = 0, e1 = 0;
-  if (valid) { e0 = ld_nc_s64(g.off + v); e1 = ld_nc_s64(g.off + v + 1); }
+  if (valid) { e0 = ld_nc_s64(g.off + ATOS_CHK(v, g.n)); e1 = ld_nc_s64(g.off + v + 1); }
   const bool is_check = valid && (t & GC_CHECK_BIT);
   const bool is_assign = valid && !(t & GC_CHECK_BIT);
   // CHECK
@@ -318,7 +318,7 @@ __device__ __forceinline__ uint32_t gc_thread_task(const GcApp& app, const Graph
       bool act = false;
       uint32_t u = 0;
       if (e < ee) {
-        u = (uint32_t)ld_stream_s32(g.col + e);
+        u = (uint32_t)ld_stream_s32(g.col + ATOS_CHK(e, g.col_cap));
         ++e;
         if (u != vg && ld_relaxed_s32(app.color + u) == c) {
           if (u < vg) self = true;
@@ -353,7 +353,7 @@ __device__ __forceinline__ uint32_t gc_thread_task(const GcApp& app, const Graph
       int64_t e = chosen < 0 ? e0 : 0, ee = chosen < 0 ? e1 : 0;
       edges += ee - e;
       for (; e < ee; ++e) {
-        const uint32_t u = (uint32_t)ld_stream_s32(g.col + e);
+        const uint32_t u = (uint32_t)ld_stream_s32(g.col + ATOS_CHK(e, g.col_cap));
         if (u == vg) continue;
         const int32_t r = ld_relaxed_s32(app.color + u) - base;
         if (r >= 0 && r < 64) m |= 1ull << r;

@@ -428,13 +428,13 @@ __global__ void k_sink_bitmap(const int64_t* off, int64_t n, uint32_t* bits) {
 
 // Hub tagging (R34), at graph create: in-degree histogram, then bit 31 of
 // every column entry whose target has in-degree >= thr, and the hub bitmap.
-__global__ void k_in_degree(const int32_t* col, int64_t m, uint32_t* indeg) {
+__global__ void k_in_degree(const int32_t* col, int64_t m, int64_t n, uint32_t* indeg) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(indeg + (col[e] & VID_MASK), 1u);
+    atomicAdd(indeg + ATOS_CHK((uint32_t)col[e] & VID_MASK, (uint32_t)n), 1u);
 }
-__global__ void k_tag_hubs(int32_t* col, int64_t m, const uint32_t* indeg, uint32_t thr) {
+__global__ void k_tag_hubs(int32_t* col, int64_t m, int64_t n, const uint32_t* indeg, uint32_t thr) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t w = (uint32_t)col[e] & VID_MASK;
+    const uint32_t w = ATOS_CHK((uint32_t)col[e] & VID_MASK, (uint32_t)n);
     col[e] = (int32_t)(w | (indeg[w] >= thr ? HUB_TAG : 0u));
   }
 }

@@ -1,5 +1,6 @@
-"""Small runs of every app x worker x kernel strategy, for compute-sanitizer
-(tests/test_queue_stress.py).  Results are checked with plain invariants
+"""Small runs of every app x worker x kernel strategy, for the bounds-checked
+library build (-DATOS_CHECKED, loaded through ATOS_LIB; tests/test_queue_stress.py)
+or a memory checker.  Results are checked with plain invariants
 (BFS grid depth = i + j, valid colouring, PageRank residues <= eps) so this
 script needs no oracle.  usage: python tools/sanitize_run.py [tool]"""
 import os
