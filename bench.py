@@ -10,15 +10,21 @@ each including its timed init (a2).  Inputs are resident in HBM before the
 timed region; the RMAT-24 CSR (1.2 GB) exceeds L2, and L2 is additionally
 flushed (512 MB write) between timed steps, outside the events.
 
-value = whole-job GTEPS = (E_bfs + E_pr) / (t_bfs + t_pr), with
+value = whole-job GTEPS_norm = (E_bfs + W_pr) / (t_bfs + t_pr), with
   E_bfs = sum of out-degrees of vertices BFS reached (Graph500 style),
-  E_pr  = edge pushes PageRank performed (GTEPS_raw).
+  W_pr  = the edge pushes of our own BSP push PageRank run (Alg. 3) on the same
+          graph at the same alpha/eps, measured once untimed (SURVEY 8d
+          GTEPS_norm, the tbl:extrawork normalisation P:818): a fixed work
+          count, so value is proportional to 1/time.  The actual edge pushes
+          are reported as pagerank.gteps_raw.
 roofline: the dominant kernel (the persistent PageRank kernel) against
 MEASURED_PEAKS.json hbm_gbs with algorithmic bytes 8 B / edge push + 32 B /
-pop, plus the same for BFS (8 B / reached edge + 28 B / vertex).
+pop, plus the same for BFS (8 B / reached edge + 28 B / vertex),
+and the sector model (32 B per random 4-B access) beside it.
 
---impl reference: the CPU oracle (oracle/, serial C) timed on this host on a
-bounded sample of the same workload (the only other place bench.py runs it).
+--impl reference: the CPU oracle (oracle/, plain C) on this host on the same
+workload, in the same unit: serial BFS + the all-cores fp64 pull-Jacobi
+PageRank time-to-answer (bounded sample; the only other place bench.py runs it).
 """
 from __future__ import annotations
 
@@ -66,9 +72,10 @@ def parse():
     return ap.parse_args()
 
 
-# returning f32 atomicAdd on random addresses of a 64 MB array, all SMs (profiles/r01_ubench.txt)
-ATOM_SKEWED_GOPS = 103.6
-ATOM_UNIFORM_GOPS = 128.2
+# returning f32 atomicAdd on random addresses of a 64 MB array, all SMs, any in-flight depth 1-16 and
+# 16-64 warps/SM (profiles/r02_ubench_sweep.md: 101.7-102.6 skewed, 125.9-127.3 uniform)
+ATOM_SKEWED_GOPS = 102.6
+ATOM_UNIFORM_GOPS = 127.3
 
 
 def peaks():
@@ -144,54 +151,119 @@ def make_graph(args):
 
 
 # ------------------------------------------------------------------ reference
+# PageRank work constant: edge pushes of our BSP push run (Alg. 3) on this workload (GTEPS_norm's
+# numerator), written by the GPU arm (pr_work_bsp) so the reference arm, which must not run
+# the CUDA path, reports in the same unit.  Not an oracle input or expected value: a unit conversion.
+WORK_FILE = os.path.join(ROOT, "profiles", "work_constants.json")
+
+
+def work_key(args):
+    return f"rmat{args.scale}_ef{args.edge_factor}_s1_a{ALPHA}_e{EPS}"
+
+
+def read_work(args):
+    try:
+        with open(WORK_FILE) as f:
+            return int(json.load(f)[work_key(args)])
+    except Exception:
+        return None
+
+
+def write_work(args, w):
+    try:
+        d = {}
+        if os.path.exists(WORK_FILE):
+            with open(WORK_FILE) as f:
+                d = json.load(f)
+        if d.get(work_key(args)) != w:
+            d[work_key(args)] = w
+            with open(WORK_FILE, "w") as f:
+                json.dump(d, f, indent=1, sort_keys=True)
+    except OSError:
+        pass
+
+
+def jacobi_sweeps_to_answer(tol=1e-10, alpha=ALPHA):
+    """Sweeps the oracle's Jacobi needs for ||x_k+1 - x_k||_1 <= tol ||x_k+1||_1: the iteration
+    contracts the L1 error by alpha per sweep (P column-substochastic), so ceil(log tol / log alpha)."""
+    import math
+    return math.ceil(math.log(tol) / math.log(alpha))
+
+
+def oracle_pagerank_answer(g, threads):
+    """Time-to-answer of the oracle's all-cores pull-Jacobi (oracle/oracle.c or_pagerank_jacobi, tol 1e-10)
+    on the full graph, from a bounded sample: calls with 2 and 10 sweeps give the per-call setup (in-edge
+    transpose) T and the per-sweep time s; answer = T + K s with K = jacobi_sweeps_to_answer()."""
+    import oracle
+    t = []
+    for k in (2, 10):
+        t0 = time.perf_counter()
+        oracle.pagerank(g, ALPHA, tol=0.0, max_iter=k, threads=threads)
+        t.append(time.perf_counter() - t0)
+    s = max((t[1] - t[0]) / 8, 1e-9)
+    T = max(t[0] - 2 * s, 0.0)
+    K = jacobi_sweeps_to_answer()
+    return T + K * s, T, s, K
+
+
 def run_reference(args, rank, world):
-    """The oracle (serial C) on this host, bounded sample of the same workload."""
+    """The oracle (plain C, oracle/) on this host, as it stands: serial FIFO BFS from 0 and the all-cores
+    fp64 pull-Jacobi PageRank, on the full workload; value in the GPU arm's unit (GTEPS_norm)."""
     if rank != 0:
         return
     import oracle
     g, _ = make_graph(args)
-    cores = 1
-    jac_iters = 2
-    times, edges = [], []
+    cores = os.cpu_count() or 1
     deg = g.degrees()
+    w_pr = read_work(args)
+    # PageRank time-to-answer: measured once (bounded sample, see oracle_pagerank_answer)
+    t_pr, T, s_sweep, K = oracle_pagerank_answer(g, cores)
+    times, edges = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         d = oracle.bfs(g, 0)
         t1 = time.perf_counter()
-        oracle.pagerank(g, ALPHA, tol=0.0, max_iter=jac_iters, threads=1)
-        t2 = time.perf_counter()
         if i >= args.warmup:
             e_bfs = int(deg[d != oracle.UNREACHED].sum())
-            times.append(t2 - t0)
-            edges.append(e_bfs + jac_iters * g.m)
+            times.append(t1 - t0 + t_pr)
+            edges.append(e_bfs + (w_pr if w_pr is not None else K * g.m))
     tot_t, tot_e = sum(times), sum(edges)
     v = tot_e / tot_t / 1e9
-    sample = (f"per step: serial FIFO BFS from 0 on the full RMAT-{args.scale} + {jac_iters} fp64 Jacobi "
-              f"PageRank sweeps (1 thread); edges = reached out-edges + {jac_iters}*m")
+    sample = (f"per step: serial FIFO BFS from 0 on the full RMAT-{args.scale} (1 thread, timed every step) + "
+              f"the all-cores ({cores} threads) fp64 pull-Jacobi time-to-answer (tol 1e-10) on the full graph, "
+              f"measured once: in-edge transpose {T:.2f} s + {K} sweeps x {s_sweep:.3f} s (sweep time from calls "
+              f"of 2 and 10 sweeps; {K} = ceil(log 1e-10 / log alpha), the contraction bound); PageRank work = "
+              + (f"our BSP push count {w_pr} (GTEPS_norm, profiles/work_constants.json)" if w_pr is not None
+                 else f"{K} x m (work constant missing)"))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_t / len(times) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_bfs0+pagerank", "scale": args.scale,
                    "edge_factor": args.edge_factor, "n": g.n, "m": g.m},
-        "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": cores, "kind": "oracle", "sample": sample,
+                         "pagerank_time_to_answer_s": t_pr, "bfs_s": statistics.mean(x - t_pr for x in times)},
         "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def cpu_baseline(g, depth_gpu, gs=None, colors_gpu=None):
+def cpu_baseline(g, depth_gpu, w_pr, gs=None, colors_gpu=None):
+    """The oracle on this host, same workload and unit as `value`: serial BFS (1 thread) + all-cores
+    Jacobi time-to-answer (bounded sample, oracle_pagerank_answer)."""
     import oracle
     deg = g.degrees()
-    jac_iters = 2
+    cores = os.cpu_count() or 1
     t0 = time.perf_counter()
     d = oracle.bfs(g, 0)
-    t1 = time.perf_counter()
-    oracle.pagerank(g, ALPHA, tol=0.0, max_iter=jac_iters, threads=1)
-    t2 = time.perf_counter()
-    e = int(deg[d != oracle.UNREACHED].sum()) + jac_iters * g.m
-    out = {"value": e / (t2 - t0) / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
-           "sample": f"serial FIFO BFS from 0 on the full graph ({t1 - t0:.1f} s) + {jac_iters} fp64 Jacobi "
-                     f"sweeps, 1 thread ({t2 - t1:.1f} s)",
+    t_bfs = time.perf_counter() - t0
+    t_pr, T, s_sweep, K = oracle_pagerank_answer(g, cores)
+    e = int(deg[d != oracle.UNREACHED].sum()) + w_pr
+    out = {"value": e / (t_bfs + t_pr) / 1e9, "unit": "GTEPS", "cores": cores, "kind": "oracle",
+           "sample": f"serial FIFO BFS from 0 on the full graph, 1 thread ({t_bfs:.2f} s) + fp64 pull-Jacobi "
+                     f"PageRank time-to-answer with {cores} threads ({t_pr:.1f} s = transpose {T:.2f} s + {K} "
+                     f"sweeps x {s_sweep:.3f} s, sweep time measured from calls of 2 and 10 sweeps; {K} = "
+                     f"ceil(log 1e-10 / log alpha)); work counted as in `value` (GTEPS_norm)",
+           "bfs_s": t_bfs, "pagerank_time_to_answer_s": t_pr, "pagerank_threads": cores,
            "bfs_matches_gpu": bool(np.array_equal(d, depth_gpu))}
     if gs is not None:
         t3 = time.perf_counter()
@@ -232,6 +304,8 @@ def run_atos(args, rank, world, local_rank):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     deg = g.degrees()
     w_pr = pr_work_bsp(atos, G)
+    if rank == 0:
+        write_work(args, w_pr)
 
     def step():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -280,6 +354,7 @@ def run_atos(args, rank, world, local_rank):
     pr_kms = statistics.mean(r[3]["kernel_ms"] for r in records)
     pr_bytes = statistics.mean(8.0 * e + 32.0 * p for e, p in zip(e_pr, pops_pr))
     pr_ach = pr_bytes / (pr_kms * 1e-3) / 1e9
+    pr_sec = statistics.mean(36.0 * e + 104.0 * p for e, p in zip(e_pr, pops_pr))
     bfs_kms = statistics.mean(r[2]["kernel_ms"] for r in records)
     bfs_bytes = 8.0 * e_bfs + 28.0 * v_bfs
     bfs_ach = bfs_bytes / (bfs_kms * 1e-3) / 1e9
@@ -298,7 +373,12 @@ def run_atos(args, rank, world, local_rank):
                      "traffic": ncu_traffic("pagerank_persistent_cta"),
                      "traffic_source": "profiles/r01_traffic.json (ncu --set full, same config)",
                      "algorithmic_bytes": pr_bytes, "kernel": "k_persistent<PrAppT<float>, CTA>",
-                     "bytes_model": "8 B/edge push + 32 B/pop", "peak_kind": peak_kind},
+                     "bytes_model": "8 B/edge push + 32 B/pop", "peak_kind": peak_kind,
+                     # SURVEY 8d sector model (diagnostic): every random 4-8 B access costs a 32-B sector
+                     "sector_model": {"bytes": pr_sec, "achieved": pr_sec / (pr_kms * 1e-3) / 1e9,
+                                      "frac": pr_sec / (pr_kms * 1e-3) / 1e9 / hbm,
+                                      "bytes_model": "36 B/edge push (col 4 + residue sector 32) + 104 B/pop "
+                                                     "(off sector 32 + slot 8 + exch sector 32 + rank sector 32)"}},
         # PageRank's edge push is one returning fp32 atomicAdd at L2 on a random, RMAT-skewed address:
         # the ceiling it actually runs against is the L2 atomic rate measured by tools/ubench.cu
         "atomic_ceiling": {"achieved_gops": statistics.mean(e / (k * 1e-3) / 1e9 for e, k in
@@ -306,10 +386,11 @@ def run_atos(args, rank, world, local_rank):
                            "peak_gops": ATOM_SKEWED_GOPS, "peak_uniform_gops": ATOM_UNIFORM_GOPS,
                            "frac": statistics.mean(e / (k * 1e-3) / 1e9 for e, k in
                                                    zip(e_pr, (r[3]["kernel_ms"] for r in records))) / ATOM_SKEWED_GOPS,
-                           "source": "profiles/r01_ubench.txt (returning f32 atomicAdd, RMAT-like skew / uniform)"},
+                           "source": "profiles/r02_ubench_sweep.md (returning f32 atomicAdd, RMAT-like skew / uniform)"},
         "bfs": {"gteps": e_bfs / (statistics.mean(t_bfs) * 1e-3) / 1e9, "ms": statistics.mean(t_bfs),
                 "kernel_ms": bfs_kms, "edges": e_bfs, "reached": v_bfs,
                 "roofline_frac": bfs_ach / hbm, "achieved_gbs": bfs_ach,
+                "sector_model_frac": (36.0 * e_bfs + 72.0 * v_bfs) / (bfs_kms * 1e-3) / 1e9 / hbm,
                 "overwork": statistics.mean(r[2]["tasks_popped"] for r in records) / max(v_exp, 1),
                 "overwork_def": "pops / reached vertices with out-degree > 0 (dangling ones are not pushed, R29)"},
         "value_def": "(BFS reached out-edges + PageRank BSP-equivalent edge pushes) / device time (GTEPS_norm, SURVEY 8d)",
@@ -328,7 +409,7 @@ def run_atos(args, rank, world, local_rank):
     if not args.no_color:
         gs, colors, out["color"] = color_leg(args, atos, dev, flush)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline(g, d_host, gs, colors)
+        out["cpu_baseline"] = cpu_baseline(g, d_host, w_pr, gs, colors)
     if rank == 0:
         print(json.dumps(out), flush=True)
 

@@ -122,6 +122,16 @@ def from_edges(n: int, edges, symmetrize: bool = False, name: str = "edges") -> 
     return _take(h, name, symmetrize)
 
 
+def fan_in(k: int, fan: int = 64) -> CSR:
+    """Fan-in hub: k sources s -> 0 and s -> s+1 (a chain, so every source has
+    out-degree 2, the last one 1), plus 0 -> 1..fan.  Vertex 0 receives k equal
+    pushes per sweep (the adversarial case for fp32 residue accumulation)."""
+    s = np.arange(1, k + 1, dtype=np.int64)
+    e = np.concatenate([np.stack([s, np.zeros(k, np.int64)], 1), np.stack([s[:-1], s[:-1] + 1], 1),
+                        np.stack([np.zeros(fan, np.int64), np.arange(1, fan + 1, dtype=np.int64)], 1)])
+    return from_edges(k + 1, e, name=f"fanin{k}")
+
+
 def permute(g: CSR, perm_seed: int):
     """Relabel by a seeded uniform permutation; returns (graph, forward) where forward[old] = new."""
     fwd = np.empty(g.n, dtype=np.int32)

@@ -92,7 +92,10 @@ typedef struct {
   int32_t hub_split;      /* persistent CTA workers: split a popped vertex with > 4096 edges into  */
                           /*   2048-edge chunk tasks (R24).  -1 = app default (BFS on, PageRank  */
                           /*   off: R33), 0 = off, 1 = on                                         */
-  int32_t _pad0;
+  int32_t pr_hub_check;   /* PageRank, persistent CTA workers with fp32 residues: hub targets    */
+                          /*   (in-degree >= 512) take fire-and-forget fp64 adds and are       */
+                          /*   activated by sweeps — this many hubs checked per processed batch */
+                          /*   (R35; default 16); 0 = threshold crossing at hubs too (R34)      */
 } atos_config;
 
 /* One timeline record per batch processed by a persistent/discrete worker:

@@ -44,8 +44,6 @@ def _load():
         lib.or_pagerank_jacobi.argtypes = [i64, vp, vp, dbl, dbl, ci, ci, vp]
         lib.or_pagerank_push.restype = ci
         lib.or_pagerank_push.argtypes = [i64, vp, vp, dbl, dbl, vp, vp, vp, vp]
-        lib.or_pagerank_residual.restype = dbl
-        lib.or_pagerank_residual.argtypes = [i64, vp, vp, dbl, vp, vp]
         lib.or_greedy_color.restype = ci
         lib.or_greedy_color.argtypes = [i64, vp, vp, vp]
         lib.or_check_bfs.restype = i64
@@ -96,13 +94,6 @@ def pagerank_push(g, alpha: float = 0.85, eps: float = 1e-6):
     if rc != 0:
         raise ValueError("or_pagerank_push failed")
     return r, s, pops.value, pushes.value
-
-
-def pagerank_residual(g, rank, alpha: float = 0.85):
-    """||T(rank) - rank||_inf diagnostic (not an acceptance gate)."""
-    n, off, col = _csr(g)
-    rk = np.ascontiguousarray(rank, dtype=np.float32)
-    return _load().or_pagerank_residual(n, off.ctypes.data, col.ctypes.data, alpha, rk.ctypes.data, None)
 
 
 def greedy_color(g):

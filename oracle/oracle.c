@@ -162,27 +162,6 @@ int or_pagerank_push(int64_t n, const int64_t* off, const int32_t* col, double a
   return 0;
 }
 
-/* T(x) - x residual diagnostic, T(x) = (1-a)1 + aPx (fp64).  Writes the     */
-/* residual vector (may be NULL) and returns ||T(x)-x||_inf.                  */
-double or_pagerank_residual(int64_t n, const int64_t* off, const int32_t* col, double alpha,
-                            const float* rank, double* out) {
-  double* t = (double*)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
-  if (!t) return -1.0;
-  for (int64_t w = 0; w < n; w++) t[w] = 1.0 - alpha;
-  for (int64_t v = 0; v < n; v++) {
-    int64_t d = off[v + 1] - off[v];
-    for (int64_t e = off[v]; e < off[v + 1]; e++) t[col[e]] += alpha * (double)rank[v] / (double)d;
-  }
-  double mx = 0;
-  for (int64_t w = 0; w < n; w++) {
-    double r = t[w] - (double)rank[w];
-    if (out) out[w] = r;
-    if (fabs(r) > mx) mx = fabs(r);
-  }
-  free(t);
-  return mx;
-}
-
 /* ---------------------------------------------------------------------- */
 /* Greedy colouring: serial first-fit in vertex-id order (the speculative    */
 /* greedy scheme of Alg. 5/6, executed without concurrency, where */

@@ -64,7 +64,7 @@ class CConfig(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("trace_capacity", ctypes.c_int64),
                 ("stage_edges", ctypes.c_int32), ("sink_defer", ctypes.c_int32),
                 ("pr_defer_degree", ctypes.c_int32), ("pr_defer_factor", ctypes.c_int32),
-                ("hub_split", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
+                ("hub_split", ctypes.c_int32), ("pr_hub_check", ctypes.c_int32)]
 
 
 class CStats(ctypes.Structure):
@@ -153,6 +153,7 @@ class Config:
     pr_defer_degree: int = 0       # PR hub deferral (R31): min out-degree; 0 = off
     pr_defer_factor: int = 4       # ... defer while residue < factor * eps
     hub_split: int = -1            # hub chunk tasks (R24): -1 app default (BFS on, PR off, R33), 0 off, 1 on
+    pr_hub_check: int = 16         # PR hubs activated by sweeps, hubs checked per batch (R35); 0 = off (R34)
 
     def to_c(self) -> CConfig:
         c = CConfig()
@@ -176,6 +177,7 @@ class Config:
         c.pr_defer_degree = self.pr_defer_degree
         c.pr_defer_factor = self.pr_defer_factor
         c.hub_split = self.hub_split
+        c.pr_hub_check = self.pr_hub_check
         s = self.stream
         if s is None:
             import torch

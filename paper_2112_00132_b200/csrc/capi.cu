@@ -177,6 +177,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->sink_defer = 1;
   c->pr_defer_degree = 0;
   c->pr_defer_factor = 4;
+  c->pr_hub_check = 16;
   c->hub_split = -1;
 }
 
@@ -202,6 +203,8 @@ static atos_status check_config(const atos_config* c) {
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "stage_edges %d not in [-1, 2^20]", c->stage_edges);
   if (c->hub_split < -1 || c->hub_split > 1)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "hub_split %d not in {-1, 0, 1}", c->hub_split);
+  if (c->pr_hub_check < 0 || c->pr_hub_check > (1 << 20))
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "pr_hub_check %d not in [0, 2^20]", c->pr_hub_check);
   if (c->pr_activation == 1 && c->check_size < 1)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "check_size < 1");
   return ATOS_OK;
@@ -314,6 +317,14 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
     g->num_hubs = (int64_t)hubs;
     if (hubs) k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, indeg, HUB_IN_DEG);
+    if (hubs) {  // R35: the hubs a PageRank sweep may activate (dangling hubs are absorbed at the end, R29)
+      CK(pool_malloc(&g->d_hub_list, (size_t)hubs * sizeof(uint32_t)));
+      CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
+      k_hub_list<<<grid_for(n, 256, g->sms), 256>>>(g->d_hub, g->d_off, n, g->d_hub_list, cnt);
+      unsigned long long nl = 0;
+      CK(cudaMemcpy(&nl, cnt, sizeof nl, cudaMemcpyDeviceToHost));
+      g->num_hub_list = (int64_t)nl;
+    }
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     pool_free(indeg);
@@ -332,6 +343,7 @@ static void graph_free(atos_graph g) {
   cudaFree(g->d_scratch);
   pool_free(g->d_sink);
   pool_free(g->d_hub);
+  pool_free(g->d_hub_list);
   Workspace& w = g->ws;
   pool_free(w.ring);
   cudaFree(w.ctl);
@@ -933,7 +945,26 @@ static atos_status pagerank_run(LaunchCtx& c, Residues<R> rs, double* rank, floa
                    c.cfg.worker == ATOS_WORKER_CTA && n <= (int64_t)DEFER_BIT;
   c.split = c.cfg.hub_split == 1;  // R33: off by default for PageRank
   PrAppT<R> app{rank, rs, (R)alpha, (R)eps, sink_bits, dfr ? (uint32_t)c.cfg.pr_defer_degree : 0u,
-                (R)eps * (R)std::max(1, c.cfg.pr_defer_factor)};
+                (R)eps * (R)std::max(1, c.cfg.pr_defer_factor), nullptr, 0u, 0u, nullptr};
+  // R35: sweep-activated hubs where the batch-closing warp runs (persistent CTA workers, fp32 residues
+  // with fp64 hubs, threshold activation elsewhere)
+  if constexpr (std::is_same<R, float>::value) {
+    if (rs.res64 && g->num_hub_list > 0 && c.cfg.pr_hub_check > 0 && c.cfg.pr_activation == 0 &&
+        c.cfg.kernel == ATOS_KERNEL_PERSISTENT && c.cfg.worker == ATOS_WORKER_CTA) {
+      PrAppT<float, true> hs{rank, rs, alpha, eps, sink_bits, app.defer_deg, app.defer_res, g->d_hub_list,
+                             (uint32_t)g->num_hub_list, (uint32_t)c.cfg.pr_hub_check, w.u32a};
+      k_hub_mark<<<fill_blocks(g->num_hub_list, g->sms), 256, 0, c.s>>>(g->d_hub_list, g->num_hub_list, w.u32a);
+      CK(cudaGetLastError());
+      c.launches++;
+      CKS((run_persistent<EdgeMapPolicy<PrAppT<float, true>>>(c, hs, make_queue(g, c.cfg, 1))));
+      if (sinks) {
+        k_pr_absorb_sinks<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(sink_bits, rs, rank, n);
+        CK(cudaGetLastError());
+        c.launches++;
+      }
+      return ATOS_OK;
+    }
+  }
   if (c.cfg.pr_activation == 1) {
     if constexpr (std::is_same<R, float>::value) {
       // f1: Alg. 4's Check_Size window activation; every vertex starts queued
@@ -1003,7 +1034,7 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
                           (unsigned long long)w.cap, (long long)n);
   CKS(ensure(w.f32a, w.f32a_n, (size_t)n));
   CKS(ensure(w.f64a, w.f64a_n, (size_t)n));
-  if (c.cfg.pr_activation == 1) CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // queued flags
+  CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // queued flags (window activation f1; hubs R35)
   CKS(ensure(w.f64b, w.f64b_n, (size_t)n));  // fp64 residues (all, or the hubs') = the seeding sums (R30)
   if (!r64) CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
   if (bsp) {

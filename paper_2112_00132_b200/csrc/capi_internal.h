@@ -48,6 +48,8 @@ struct atos_graph_s {
   uint32_t* d_sink = nullptr;  // bit v = (deg(v) == 0), built at create (R29)
   uint32_t* d_hub = nullptr;   // bit v = in-degree >= HUB_IN_DEG; columns carry HUB_TAG (R34); nullptr = untagged
   int64_t num_hubs = 0;
+  uint32_t* d_hub_list = nullptr;  // hub vertex ids with out-degree > 0 (R35 sweep activation)
+  int64_t num_hub_list = 0;
   void* d_scratch = nullptr;
   bool owned = false;
   bool symmetric = false;

@@ -51,12 +51,100 @@ __device__ __forceinline__ void warp_exclusive_scan(int64_t* a, int n) {
 #define ATOS_AGENT_G 2
 #endif
 constexpr int AGENT_G = ATOS_AGENT_G;
+// Phase 0 (slot reads) holds one u64 per item, so it takes more items per L2
+// round trip than the later phases.
+#ifndef ATOS_AGENT_SLOT_G
+#define ATOS_AGENT_SLOT_G 2
+#endif
+constexpr int AGENT_SLOT_G = ATOS_AGENT_SLOT_G;
 
 // Apps that may defer a popped task (PageRank hub deferral, R31) declare kDefer.
 template <class A, class = void>
 struct DeferTrait : std::false_type {};
 template <class A>
 struct DeferTrait<A, std::void_t<decltype(A::kDefer)>> : std::integral_constant<bool, A::kDefer> {};
+
+// Apps with sweep-activated hubs (PageRank R35) declare kHubSweep.
+template <class A, class = void>
+struct HubSweepTrait : std::false_type {};
+template <class A>
+struct HubSweepTrait<A, std::void_t<decltype(A::kHubSweep)>> : std::integral_constant<bool, A::kHubSweep> {};
+
+// R35 sweep step (warp-collective; the warp that closes a batch, before its
+// q_done, so the pushes are reserved while the batch still counts as
+// unprocessed — a7): check app.hub_check hubs from the round-robin cursor
+// ctl->aux[0] and push those whose fp64 residue exceeds eps and that are not
+// queued (hq 0 -> 1).  Returns the pushes (warp-uniform).
+template <class App>
+__device__ __forceinline__ uint32_t hub_sweep(const App& app, const Queue& q) {
+  uint64_t s = 0;
+  if (lane_id() == 0)
+    s = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->aux[0].v), (unsigned long long)app.hub_check);
+  s = __shfl_sync(FULL_MASK, s, 0);
+  uint32_t pushed = 0;
+  for (uint32_t i = 0; i < app.hub_check; i += 32 * AGENT_G) {
+    uint32_t v[AGENT_G];
+    double r[AGENT_G];
+#pragma unroll
+    for (int k = 0; k < AGENT_G; ++k) {
+      const uint32_t j = i + lane_id() + 32 * k;
+      v[k] = j < app.hub_check ? __ldg(app.hubs + (uint32_t)((s + j) % app.num_hubs)) : 0xFFFFFFFFu;
+      r[k] = v[k] != 0xFFFFFFFFu ? __ldcg(app.rs.res64 + v[k]) : 0.0;
+    }
+    bool act[AGENT_G];
+#pragma unroll
+    for (int k = 0; k < AGENT_G; ++k)
+      act[k] = r[k] > (double)app.eps && ld_relaxed_u32(app.hq + v[k]) == 0u && atomicExch(app.hq + v[k], 1u) == 0u;
+    pushed += q_warp_push_multi<AGENT_G>(q, act, v);
+  }
+  return pushed;
+}
+
+// R35 termination (R9's clean-sweep protocol over the hubs): called by an
+// idle agent warp that saw the queue quiescent (processed == tail == t0).
+// One warp at a time (lock ctl->aux[3]: 0 free, 1 sweeping, 2 done) checks
+// EVERY hub and pushes each with residue > eps (flags are ignored: with the
+// queue quiescent no copy is queued).  Returns 2 = the run is over (a clean
+// sweep with the queue unchanged), 1 = it pushed or the queue moved (keep
+// popping), 0 = another warp holds the lock (poll again).
+template <class App>
+__device__ __forceinline__ int hub_final_sweep(const App& app, const Queue& q, uint64_t t0) {
+  int state = 0;
+  if (lane_id() == 0) {
+    const uint64_t flag = ld_relaxed_u64(&q.ctl->aux[3].v);
+    if (flag == 2) state = 2;
+    else if (atomicCAS(reinterpret_cast<unsigned long long*>(&q.ctl->aux[3].v), 0ull, 1ull) == 0ull) state = 1;
+  }
+  state = __shfl_sync(FULL_MASK, state, 0);
+  if (state != 1) return state;
+  uint32_t found = 0;
+  for (uint32_t b = 0; b < app.num_hubs; b += 32 * AGENT_G) {
+    uint32_t v[AGENT_G];
+    double r[AGENT_G];
+#pragma unroll
+    for (int k = 0; k < AGENT_G; ++k) {
+      const uint32_t j = b + lane_id() + 32 * k;
+      v[k] = j < app.num_hubs ? __ldg(app.hubs + j) : 0xFFFFFFFFu;
+      r[k] = v[k] != 0xFFFFFFFFu ? __ldcg(app.rs.res64 + v[k]) : 0.0;
+    }
+    bool act[AGENT_G];
+#pragma unroll
+    for (int k = 0; k < AGENT_G; ++k) {
+      act[k] = r[k] > (double)app.eps;
+      if (act[k]) atomicExch(app.hq + v[k], 1u);
+    }
+    found += q_warp_push_multi<AGENT_G>(q, act, v);
+  }
+  bool done = false;
+  if (lane_id() == 0) {
+    __threadfence();
+    const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
+    const uint64_t t = q_enqueued(q);
+    done = found == 0 && p == t && t == t0;
+    st_relaxed_u64(&q.ctl->aux[3].v, done ? 2ull : 0ull);
+  }
+  return __shfl_sync(FULL_MASK, done, 0) ? 2 : 1;
+}
 
 // Per-item state of a batch between the agent's phases, kept in pre[i]:
 // a vertex item (>= 0, may carry DEFER_BIT), a resolved chunk task
@@ -107,15 +195,15 @@ __device__ __forceinline__ uint32_t agent_prepare(const App& app, const GraphVie
   // be released for its next lap (ring wrap-around) never waits on this agent
   // (the agent used to push between sub-rounds of unread claims).
   bool pending = false;
-  for (uint32_t base = 0; base < n; base += 32 * AGENT_G) {
-    uint64_t raw[AGENT_G];
+  for (uint32_t base = 0; base < n; base += 32 * AGENT_SLOT_G) {
+    uint64_t raw[AGENT_SLOT_G];
 #pragma unroll
-    for (int k = 0; k < AGENT_G; ++k) {
+    for (int k = 0; k < AGENT_SLOT_G; ++k) {
       const uint32_t i = base + lane + 32 * k;
       raw[k] = i < n ? ld_relaxed_u64(q.ring + ((first + i) & q.mask)) : 0;
     }
 #pragma unroll
-    for (int k = 0; k < AGENT_G; ++k) {
+    for (int k = 0; k < AGENT_SLOT_G; ++k) {
       const uint32_t i = base + lane + 32 * k;
       if (i < n && !agent_take(app, q, first + i, raw[k], i, e0s, pre, pay)) {
         pre[i] = STASH_PENDING;

@@ -24,6 +24,14 @@ namespace atos {
 #define ATOS_NBUF 4
 #endif
 constexpr int NBUF = ATOS_NBUF;
+// Queue-agent warps per CTA (build-time): agent a prepares ring batches
+// i = a, a + AGENTS, ... (buffer i % NBUF); workers consume every batch in
+// order and skip the batches of an agent that has published QUIT.
+#ifndef ATOS_AGENTS
+#define ATOS_AGENTS 1
+#endif
+constexpr int AGENTS = ATOS_AGENTS;
+static_assert(NBUF % AGENTS == 0, "NBUF must be a multiple of AGENTS");
 constexpr int STEP_CAP = 512;  // per-buffer step-owner table (u16; steps beyond it binary-search)
 // Register budget vs occupancy of the persistent CTA kernel (build-time knobs).
 // Measured on RMAT-24 (PR kernel ms / BFS ms): 1024x1 bound (64 regs, some
@@ -99,16 +107,19 @@ __host__ __device__ constexpr size_t ws2_smem_bytes(int F, int S) {
 __device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
 __device__ __forceinline__ void vstore(int* p, int v) { *(volatile int*)p = v; }
 
-// Agent pop from the global queue; the idle path runs the termination check (a7).
-__device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& hw,
-                                              long long& last_count) {
+// Agent pop from the global queue; the idle path runs the termination check
+// (a7) — for apps with sweep-activated hubs (R35) quiescence must also pass a
+// clean hub sweep.
+template <class App>
+__device__ __forceinline__ uint32_t agent_pop(const App& app, const Queue& q, uint32_t want, uint64_t& first,
+                                              uint64_t& hw, long long& last_count) {
   const int lane = lane_id();
   unsigned ns = 0;
   for (;;) {
     // abort / watchdog are checked on the idle path only
     uint32_t n = 0;
-    uint64_t qlen = 0;
-    bool quit = false;
+    uint64_t qlen = 0, t = 0;
+    bool quit = false, quiescent = false;
     if (lane == 0) {
       n = q_try_pop(q, want, first, qlen, last_count);
       last_count = (long long)qlen - (long long)n;
@@ -118,14 +129,23 @@ __device__ __forceinline__ uint32_t agent_pop(const Queue& q, uint32_t want, uin
         quit = true;
       } else {
         const uint64_t p = ld_acquire_u64(&q.ctl->processed.v);
-        const uint64_t t = q_enqueued(q);
-        quit = p == t;
+        t = q_enqueued(q);
+        quiescent = p == t;
       }
     }
     n = __shfl_sync(FULL_MASK, n, 0);
     first = __shfl_sync(FULL_MASK, first, 0);
     if (n) return n;
     if (__shfl_sync(FULL_MASK, quit, 0)) return 0;
+    if (__shfl_sync(FULL_MASK, quiescent, 0)) {
+      if constexpr (HubSweepTrait<App>::value) {
+        const int r = hub_final_sweep(app, q, __shfl_sync(FULL_MASK, t, 0));
+        if (r == 2) return 0;
+        if (r == 1) { ns = 0; continue; }
+      } else {
+        return 0;
+      }
+    }
     if (ns) __nanosleep(ns);
     ns = ns == 0 ? 32 : (ns < q.backoff_ns ? ns * 2 : ns);
   }
@@ -182,7 +202,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
   auto buf_sofs = [&](int b) { return reinterpret_cast<int*>(smem + b * bb + ws2_sofs_offset<Payload>(F)); };
   auto buf_stage = [&](int b) { return reinterpret_cast<int32_t*>(smem + b * bb + ws2_stage_offset<Payload>(F)); };
   const Queue* cq = q.chunks ? &q : nullptr;
-  const int nw = (T >> 5) - 1;
+  const int nw = (T >> 5) - AGENTS;
   if (tid < NBUF) {
     hdr[tid] = BufHdr{BUF_FREE, -1, 0, 0, 0, 0, 0};
     if (S) mbar_init(&bars[tid], 1);
@@ -190,11 +210,11 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
   if (S && tid == 0) fence_mbar_init();
   __syncthreads();
 
-  if (wid == 0) {
-    // ------------------------------------------------ queue agent
+  if (wid < AGENTS) {
+    // ------------------------------------------------ queue agent(s)
     long long last_count = 0;  // lane 0: queue length seen at the last pop
     WPROF_DECL
-    for (int i = 0;; ++i) {
+    for (int i = wid;; i += AGENTS) {
       const int b = i % NBUF;
       // wait until the workers have released buffer b
       bool dead = false;
@@ -213,7 +233,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       if constexpr (App::kWindow) {
         n = window_pop(app, q, (uint32_t)F, first, st.hw);
       } else {
-        n = agent_pop(q, (uint32_t)F, first, st.hw, last_count);
+        n = agent_pop(app, q, (uint32_t)F, first, st.hw, last_count);
       }
       WPROF_MARK(1);
       if (n) {
@@ -250,17 +270,23 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
     RingSink sink{q};
     uint32_t pushed = 0;
     uint64_t edges = 0;
+    unsigned quit_mask = 0;  // agents that have published QUIT
     WPROF_DECL
     for (int i = 0;; ++i) {
       const int b = i % NBUF, pass = i / NBUF;
+      if ((quit_mask >> (i % AGENTS)) & 1u) continue;
       int s = BUF_FREE;
       for (unsigned ns = 8;; ns = ns < 128 ? ns * 2 : ns) {
         s = vload(&hdr[b].state);
         if (s != BUF_FREE && vload(&hdr[b].seq) == pass) break;
         __nanosleep(ns);
-        if (ns >= 128 && (q_aborted(q) || q_timed_out(q))) { s = BUF_QUIT; break; }
+        if (ns >= 128 && (q_aborted(q) || q_timed_out(q))) { s = BUF_QUIT; quit_mask = (1u << AGENTS) - 1; break; }
       }
-      if (s == BUF_QUIT) break;
+      if (s == BUF_QUIT) {
+        quit_mask |= 1u << (i % AGENTS);
+        if (quit_mask == (1u << AGENTS) - 1) break;
+        continue;
+      }
       __threadfence_block();
       // this batch's staged columns complete the buffer's pass-th mbarrier phase
       if (S) {
@@ -304,6 +330,9 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
         last = atomicAdd(&hdr[b].left, 1) == nw - 1;
       }
       last = __shfl_sync(FULL_MASK, last, 0);
+      if constexpr (HubSweepTrait<App>::value) {
+        if (last) pushed += hub_sweep(app, q);  // R35, before this batch's q_done
+      }
       if (last && lane == 0) {
         st.popped += (uint64_t)n;
         if constexpr (App::kWindow) {

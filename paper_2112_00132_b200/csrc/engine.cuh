@@ -193,7 +193,7 @@ struct Residues {
 // r = atomicExch(res[v], 0); rank[v] += r; c = alpha r / deg(v);
 // per edge: old = atomicAdd(res[w], c); push w iff old <= eps < old + c.
 // rank accumulates in fp64 (a per-pop cost): a hub receives 10^4+ pops.
-template <class R>
+template <class R, bool HS = false>
 struct PrAppT {
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
@@ -211,8 +211,21 @@ struct PrAppT {
   // so it comes back with the residue accumulated over a second queue cycle
   // instead of scattering an eps-sized residue over thousands of edges.
   static constexpr bool kDefer = true;
+  static constexpr bool kHubSweep = HS;
   uint32_t defer_deg;  // 0 = off
   R defer_res;
+  // Sweep activation of hubs (R35, persistent CTA workers; HS = true):
+  // an edge push to a hub target (column HUB_TAG) is a fire-and-forget fp64
+  // `red` with no threshold test, and hubs are activated instead by sweeps —
+  // the worker warp that closes a batch checks hub_check hubs of `hubs` (a
+  // round-robin cursor) and pushes those with residue > eps not already
+  // queued (hq[v] = 1 while a copy is queued; cleared at pop).  With the queue
+  // quiescent one warp sweeps every hub (hub_final_sweep) and the run ends
+  // only after a clean sweep (R9's protocol over the hubs alone).
+  const uint32_t* hubs;
+  uint32_t num_hubs;
+  uint32_t hub_check;
+  uint32_t* hq;
   using Payload = R;
   using Probe = uint32_t;  // the column's hub tag
   using Raw = double;
@@ -244,6 +257,11 @@ struct PrAppT {
     return x;
   }
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
+    // R35: a popped hub is no longer queued; a sweep may re-queue it as soon as
+    // its residue exceeds eps again (an extra copy only pops a small residue)
+    if constexpr (HS) {
+      if ((x.t.word >> (v & 31)) & 1u) atomicExch(hq + v, 0u);
+    }
     const double r = rs.take_finish(v, x.t);
     if (r == 0.0) return false;
     red_add_cold(rank + v, r);
@@ -253,8 +271,19 @@ struct PrAppT {
     return true;
   }
   __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
-  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const { return rs.add(w, tag, c); }
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
+    if constexpr (HS) {
+      if (tag) {  // R35: hub target, activated by sweeps
+        red_add_hot(rs.res64 + w, (double)c);
+        return 0.0;
+      }
+    }
+    return rs.add(w, tag, c);
+  }
   __device__ __forceinline__ bool decide(Payload c, uint32_t w, Probe tag, Raw old) const {
+    if constexpr (HS) {
+      if (tag) return false;
+    }
     if (!rs.crossed(tag, old, c, eps)) return false;
     return !test_bit(sink, w);
   }

@@ -450,6 +450,26 @@ __global__ void k_hub_bitmap(const uint32_t* indeg, int64_t n, uint32_t thr, uin
   }
 }
 
+// R35: list of hub vertices with out-degree > 0, in id order within each warp's 32 ids.
+__global__ void k_hub_list(const uint32_t* bits, const int64_t* off, int64_t n, uint32_t* list,
+                           unsigned long long* count) {
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = b + lane_id();
+    const bool h = v < n && ((bits[v >> 5] >> (v & 31)) & 1u) && off[v + 1] > off[v];
+    const uint32_t m = __ballot_sync(FULL_MASK, h);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(FULL_MASK, base, 0);
+    if (h) list[base + __popc(m & lanemask_lt())] = (uint32_t)v;
+  }
+}
+// R35: every listed hub starts queued (the initial queue holds all vertices)
+__global__ void k_hub_mark(const uint32_t* list, int64_t k, uint32_t* hq) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    hq[list[i]] = 1u;
+}
+
 // Sink absorption (R29): after quiescence every dangling vertex performs its
 // deferred task body `rank[v] += exch(res[v], 0)` (Alg. 4 line 8 with deg 0, R5).
 template <class R>
