@@ -137,7 +137,7 @@ class ClockSampler:
 def ncu_traffic(key):
     """Per-launch DRAM traffic of a kernel from the committed ncu capture (profiles/), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             return json.load(f)[key]["bytes"]
     except Exception:
         return None
@@ -371,8 +371,8 @@ def run_atos(args, rank, world, local_rank):
                    "parallelism": "replicas" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": pr_ach, "peak": hbm, "unit": "GB/s", "frac": pr_ach / hbm,
                      "traffic": ncu_traffic("pagerank_persistent_cta"),
-                     "traffic_source": "profiles/r01_traffic.json (ncu --set full, same config)",
-                     "algorithmic_bytes": pr_bytes, "kernel": "k_persistent<PrAppT<float>, CTA>",
+                     "traffic_source": "profiles/r02_traffic.json (ncu --set full, same config)",
+                     "algorithmic_bytes": pr_bytes, "kernel": "k_persistent<PrAppT<float, true>, CTA>",
                      "bytes_model": "8 B/edge push + 32 B/pop", "peak_kind": peak_kind,
                      # SURVEY 8d sector model (diagnostic): every random 4-8 B access costs a 32-B sector
                      "sector_model": {"bytes": pr_sec, "achieved": pr_sec / (pr_kms * 1e-3) / 1e9,

@@ -15,7 +15,7 @@
  *  - Calls are synchronous: outputs are complete when the call returns.
  *  - One call at a time per graph handle; distinct handles used from distinct
  *    host threads on distinct streams are independent.
- *  - Vertex ids are 32-bit: n must be < 2^31 - 1 (bit 31 tags colouring CHECK
+ *  - Vertex ids are 32-bit: n must be < 2^30 - 1 (bits 30-31 of a column entry are tags, R37; bit 31 tags colouring CHECK
  *    tasks, R10).  Edge offsets are 64-bit.
  *  - Output buffers are caller-allocated with n entries and may live in host
  *    or device memory (detected with cudaPointerGetAttributes).  They are fully
@@ -39,7 +39,7 @@ typedef enum {
   ATOS_ERR_NCCL = 5,             /* NCCL error or NCCL library not loadable          */
   ATOS_ERR_QUEUE_OVERFLOW = 6,   /* more live tasks than queue_capacity */
   ATOS_ERR_TIMEOUT = 7,          /* device watchdog fired (timeout_s exceeded)        */
-  ATOS_ERR_UNSUPPORTED = 8       /* e.g. n >= 2^31-1, or an option not built          */
+  ATOS_ERR_UNSUPPORTED = 8       /* e.g. n >= 2^30-1, or an option not built          */
 } atos_status;
 
 typedef struct atos_graph_s* atos_graph; /* opaque; owns (or borrows) a device CSR */
@@ -138,7 +138,7 @@ void atos_config_default(atos_config* cfg);
  * ATOS_GRAPH_BORROW|ATOS_GRAPH_DEVICE_PTRS.  A copied CSR gets hub tags (bit
  * 31 of a column entry = its target's in-degree is >= 512, R34; internal to
  * the library).  m may exceed 2^31.  n == 0 is allowed.  Errors: INVALID_ARGUMENT (n<0, m<0, NULL pointers with m>0, out==NULL),
- * UNSUPPORTED (n >= 2^31-1), INVALID_GRAPH (with VALIDATE), OUT_OF_MEMORY, CUDA. */
+ * UNSUPPORTED (n >= 2^30-1), INVALID_GRAPH (with VALIDATE), OUT_OF_MEMORY, CUDA. */
 atos_status atos_graph_create(const int64_t* row_offsets, const int32_t* col_indices, int64_t n,
                               int64_t m, uint32_t flags, atos_graph* out);
 atos_status atos_graph_destroy(atos_graph g);
@@ -250,6 +250,28 @@ atos_status atos_comm_destroy(atos_comm c);
 atos_status atos_graph_create_partitioned(atos_comm c, int64_t global_n, int64_t v_begin, int64_t v_end,
                                           const int64_t* local_row_offsets, const int32_t* col_global,
                                           int64_t local_m, uint32_t flags, atos_graph* out);
+
+/* ---------------- asynchronous peer-memory partitions ----------------
+ * The same 1-D vertex split as above, but with no exchange rounds (PAPER.md
+ * P:99): partition p = global ids [p*n/parts, (p+1)*n/parts) (callers
+ * permute first) keeps its CSR rows, per-vertex state and task queue on
+ * devices[p]; a worker relaxing an edge into another partition's vertex
+ * updates that vertex's state in place (atomicMin / fp64 atomicAdd through a
+ * peer pointer) and pushes it onto the owner's queue (remote warp-aggregated
+ * push); termination = equal sums of every queue's processed and tail
+ * counters (read in that order).  devices NULL = every partition on the
+ * current device, run as ONE persistent kernel whose blocks are split among
+ * the partitions; otherwise devices must be pairwise distinct with peer
+ * access (one persistent kernel per device, launched together).  Host CSR
+ * only (copied); VALIDATE honoured.  atos_bfs / atos_pagerank (threshold
+ * activation, fp64 residues, warp workers of FETCH_SIZE; kernel / worker
+ * fields ignored) write all n outputs; atos_color returns UNSUPPORTED.
+ * Errors: INVALID_ARGUMENT (parts not in [1, 8], n < parts, devices neither
+ * all equal nor all distinct), UNSUPPORTED (no peer access, device pointers,
+ * n >= 2^30-1), INVALID_GRAPH, OUT_OF_MEMORY, CUDA. */
+atos_status atos_graph_create_peer(int32_t parts, const int32_t* devices, const int64_t* row_offsets,
+                                   const int32_t* col_indices, int64_t n, int64_t m, uint32_t flags,
+                                   atos_graph* out);
 
 /* Graph-lifetime device memory comes from a private stream-ordered pool that
  * keeps up to 8 GB of freed memory mapped for reuse by the next graph

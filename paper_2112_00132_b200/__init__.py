@@ -38,7 +38,7 @@ EXPORTS = [
     "atos_config_default", "atos_graph_create", "atos_graph_destroy", "atos_graph_info", "atos_bfs",
     "atos_pagerank", "atos_color", "atos_status_string", "atos_last_error", "atos_version",
     "atos_comm_unique_id", "atos_comm_init", "atos_comm_init_host", "atos_comm_info", "atos_comm_destroy",
-    "atos_graph_create_partitioned", "atos_pool_trim", "atos_pool_reserved",
+    "atos_graph_create_partitioned", "atos_graph_create_peer", "atos_pool_trim", "atos_pool_reserved",
 ]
 
 # callback types of atos_comm_init_host (include/atos.h)
@@ -109,11 +109,13 @@ def lib():
         L.atos_comm_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
         L.atos_comm_destroy.argtypes = [vp]
         L.atos_graph_create_partitioned.argtypes = [vp, i64, i64, i64, vp, vp, i64, u32, ctypes.POINTER(vp)]
+        L.atos_graph_create_peer.argtypes = [i32, vp, vp, vp, i64, i64, u32, ctypes.POINTER(vp)]
         L.atos_pool_trim.argtypes = [ctypes.c_uint64]
         L.atos_pool_reserved.argtypes = [ctypes.POINTER(ctypes.c_uint64)]
         for f in ("atos_graph_create", "atos_graph_destroy", "atos_graph_info", "atos_bfs", "atos_pagerank",
                   "atos_color", "atos_comm_unique_id", "atos_comm_init", "atos_comm_init_host", "atos_comm_info",
-                  "atos_comm_destroy", "atos_graph_create_partitioned", "atos_pool_trim", "atos_pool_reserved"):
+                  "atos_comm_destroy", "atos_graph_create_partitioned", "atos_graph_create_peer", "atos_pool_trim",
+                  "atos_pool_reserved"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -251,6 +253,26 @@ class Graph:
         self.symmetric = symmetric
         if not is_t:
             self._keep = None  # copied; host arrays may be freed
+
+    @classmethod
+    def peer(cls, off, col, parts: int, devices=None, validate: bool = False):
+        """Asynchronous peer-memory partitions (atos_graph_create_peer): `parts`
+        contiguous vertex blocks on `devices` (None: all on the current device, one launch over
+        every partition).  atos_bfs / atos_pagerank run with no exchange rounds."""
+        self = cls.__new__(cls)
+        off = np.ascontiguousarray(off, dtype=np.int64)
+        col = np.ascontiguousarray(col, dtype=np.int32)
+        dv = None if devices is None else np.ascontiguousarray(devices, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _check(lib().atos_graph_create_peer(parts, dv.ctypes.data if dv is not None else None, off.ctypes.data,
+                                            col.ctypes.data if col.size else None, off.shape[0] - 1, col.shape[0],
+                                            GRAPH_VALIDATE if validate else 0, ctypes.byref(h)),
+               "atos_graph_create_peer")
+        self._keep = None
+        self.h = h
+        self.n, self.m = int(off.shape[0] - 1), int(col.shape[0])
+        self.symmetric = False
+        return self
 
     @classmethod
     def from_csr(cls, g, **kw):

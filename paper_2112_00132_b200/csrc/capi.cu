@@ -181,7 +181,18 @@ extern "C" void atos_config_default(atos_config* c) {
   c->hub_split = -1;
 }
 
+#ifndef ATOS_BACKOFF_NS
+#define ATOS_BACKOFF_NS 256  // idle-poll backoff cap (ns) of queue poppers
+#endif
+
 static atos_status check_failures();
+
+// asynchronous peer-memory partitions (peer_impl.cuh)
+struct PeerState;
+static atos_status peer_bfs(atos_graph g, int64_t src, const atos_config& cfg, uint32_t* depth_out, atos_stats* st);
+static atos_status peer_pagerank(atos_graph g, float alpha, float eps, const atos_config& cfg, float* rank_out,
+                                 atos_stats* st);
+static void peer_free(PeerState* ps);
 
 static atos_status check_config(const atos_config* c) {
   if (c->struct_size != sizeof(atos_config))
@@ -316,7 +327,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     unsigned long long hubs = 0;
     CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
     g->num_hubs = (int64_t)hubs;
-    if (hubs) k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, indeg, HUB_IN_DEG);
+    k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, indeg, HUB_IN_DEG, g->d_sink);
     if (hubs) {  // R35: the hubs a PageRank sweep may activate (dangling hubs are absorbed at the end, R29)
       CK(pool_malloc(&g->d_hub_list, (size_t)hubs * sizeof(uint32_t)));
       CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
@@ -336,6 +347,11 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
 
 static void graph_free(atos_graph g) {
   if (!g) return;
+  if (g->peer) {
+    peer_free(g->peer);
+    delete g;
+    return;
+  }
   if (g->owned) {
     pool_free(g->d_off);
     pool_free(g->d_col);
@@ -372,7 +388,8 @@ extern "C" atos_status atos_graph_create(const int64_t* off, const int32_t* col,
   *out = nullptr;
   if (n < 0 || m < 0) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "n < 0 or m < 0");
   if (!off || (m > 0 && !col)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "NULL CSR pointer");
-  if (n >= 0x7FFFFFFFLL) return atos_set_error(ATOS_ERR_UNSUPPORTED, "n >= 2^31-1 (bit 31 tags colouring tasks)");
+  if (n >= (int64_t)VID_MASK)
+    return atos_set_error(ATOS_ERR_UNSUPPORTED, "n >= 2^30-1 (bits 30-31 of a column entry are tags, R37)");
   atos_graph g = new (std::nothrow) atos_graph_s();
   if (!g) return atos_set_error(ATOS_ERR_OUT_OF_MEMORY, "host allocation");
   atos_status s = graph_init_common(g, off, col, n, m, flags, n);
@@ -431,16 +448,23 @@ atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, ui
       pool_free(w.ring);
       w.ring = nullptr;
       CK(pool_malloc(&w.ring, cap * sizeof(uint64_t)));
-      CK(cudaMemsetAsync(w.ring, 0, cap * sizeof(uint64_t), s));
       w.cap = cap;
-      w.dirty = 0;
-    } else if (w.dirty) {
-      CK(cudaMemsetAsync(w.ring, 0, std::min<uint64_t>(w.dirty, cap) * sizeof(uint64_t), s));
-      w.dirty = 0;
+      w.clear = cap;
+    } else {
+      w.clear = std::min<uint64_t>(w.dirty, cap);
     }
     w.dirty = cap;  // unknown until this run finishes cleanly (finish_stats narrows it)
   }
   (void)n_local;
+  return ATOS_OK;
+}
+
+// Zero the ring slots the last run used (w.clear, set by ws_prepare), on the
+// call's stream INSIDE the timed region (after ev[0]): a clean ring is part of
+// every run's init (a2).
+static atos_status ring_reset(Workspace& w, cudaStream_t s) {
+  if (w.ring && w.clear) CK(cudaMemsetAsync(w.ring, 0, w.clear * sizeof(uint64_t), s));
+  w.clear = 0;
   return ATOS_OK;
 }
 
@@ -455,7 +479,7 @@ static Queue make_queue(atos_graph g, const atos_config& cfg, uint32_t kind) {
   q.timeout_ns = cfg.timeout_s > 0 ? (uint64_t)(cfg.timeout_s * 1e9) : 0;
   q.head_floor = 0;
   q.trace_kind = kind;
-  q.backoff_ns = 256;
+  q.backoff_ns = ATOS_BACKOFF_NS;
   q.trace = reinterpret_cast<TraceRec*>(cfg.trace);
   q.trace_cap = cfg.trace ? (uint64_t)cfg.trace_capacity : 0;
   return q;
@@ -562,8 +586,10 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
   }
   size_t smem = worker_smem_bytes<P>(W, F, T, true);
   if (smem > 227 * 1024) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "fetch_size %d x cta_threads %d needs %zu B shared memory (> 227 KB)", F, c.cfg.cta_threads, smem);
-  if (W == W_CTA && P::kWarpSpecialised && T < 64)
-    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "persistent CTA workers need cta_threads >= 64 (1 queue warp + workers)");
+  constexpr int agents = AgentsTrait<App>::value;
+  if (W == W_CTA && P::kWarpSpecialised && T < 32 * (agents + 1))
+    return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "persistent CTA workers of this app need cta_threads >= %d "
+                          "(%d queue-agent warp(s) + workers)", 32 * (agents + 1), agents);
   CKS(set_smem(kern, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
@@ -854,6 +880,7 @@ static atos_status part_call(LaunchCtx& c, int app, int64_t src, float alpha, fl
 extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t* depth_out, atos_stats* st) {
   LaunchCtx c;
   CKS(begin_call(g, cfg, c, st));
+  if (g->peer) return peer_bfs(g, src, c.cfg, depth_out, st);
   if (g->dist) {
     if (src < 0 || src >= g->global_n)
       return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "src %lld not in [0, %lld)", (long long)src, (long long)g->global_n);
@@ -874,13 +901,15 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
     CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
   }
   CK(cudaEventRecord(w.ev[0], c.s));
+  CKS(ring_reset(w, c.s));
   // a2: init (timed)
   k_bfs_init<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, w.u32b, w.u16a, n, src);
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : 1, w.ring, bsp ? -1 : src);
   CK(cudaGetLastError());
   c.launches += 2;
   CK(cudaEventRecord(w.ev[1], c.s));
-  BfsApp app{w.u32a, w.u32b, w.u16a, c.cfg.bfs_filter, c.cfg.sink_defer ? g->d_sink : nullptr};
+  BfsApp app{w.u32a, w.u32b, w.u16a, c.cfg.bfs_filter, c.cfg.sink_defer ? g->d_sink : nullptr,
+             g->d_hub != nullptr ? 1u : 0u};
   c.split = c.cfg.hub_split != 0;  // R24: on by default for BFS
   using P = EdgeMapPolicy<BfsApp>;
   if (c.cfg.kernel == ATOS_KERNEL_PERSISTENT) {
@@ -916,42 +945,51 @@ static atos_status pagerank_run(LaunchCtx& c, Residues<R> rs, double* rank, floa
   const int64_t n = g->n;
   const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
   CK(cudaEventRecord(w.ev[0], c.s));
+  CKS(ring_reset(w, c.s));
   // a2: rank = 1 - alpha ; residue seeded by one synchronous push (R4) ; all vertices enqueued
   k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rank, n, 1.0 - (double)alpha);
   // R30: the seeding sums accumulate in fp64 (w.f64b: the hub residues, or every residue when R = double)
   // and are rounded once to fp32 for non-hubs: fp32 adds of one repeated c = (1-a)a/deg(v) onto a hub's
   // growing sum round with correlated errors (measured: RMAT-27's hub 4.8e-4 of max x* low)
-  double* acc = w.f64b;
-  k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, n, 0.0);
+  const bool f32 = !std::is_same<R, double>::value;
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
-  {
+  LaunchCtx ci = c;
+  ci.cfg.worker = ATOS_WORKER_CTA;
+  if constexpr (std::is_same<R, float>::value) {
+    // tagged graph: fp32 sums for non-hubs, fp64 at hubs (PrInitSplitApp)
+    k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rs.res, n, 0.f);
+    k_zero_hubs<<<fill_blocks((n + 31) / 32, g->sms), 256, 0, c.s>>>(rs.hub, n, rs.res64);
+    PrInitSplitApp ia{rs.res, rs.res64, (1.0 - (double)alpha) * (double)alpha};
+    CKS((bsp_step_w<EdgeMapPolicy<PrInitSplitApp>, PrInitSplitApp, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr,
+                                                                         nullptr, 256, nullptr)));
+  } else {
+    double* acc = w.f64b;  // every residue fp64: the sums are the residues
+    k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, n, 0.0);
     PrInitAppT<double> ia{acc, (1.0 - (double)alpha) * (double)alpha};
-    LaunchCtx ci = c;
-    ci.cfg.worker = ATOS_WORKER_CTA;
     CKS((bsp_step_w<EdgeMapPolicy<PrInitAppT<double>>, PrInitAppT<double>, W_CTA>(ci, ia, nullptr, (uint64_t)n,
                                                                                  nullptr, nullptr, 256, nullptr)));
   }
-  const bool f32 = !std::is_same<R, double>::value;
-  if (f32) k_f64_to_res<R><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, rs.res, rs.hub, n);
   if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
   // R29: sink deferral for the threshold-activated queue strategies
   const bool sinks = c.cfg.sink_defer && !bsp && c.cfg.pr_activation == 0;
   const uint32_t* sink_bits = sinks ? g->d_sink : nullptr;
   CK(cudaGetLastError());
-  c.launches += (bsp ? 4 : 5) + (f32 ? 1 : 0);
+  c.launches += (bsp ? 4 : 5) + (f32 ? 1 : 0);  // fills, ctl, seeding, (hub zeroing), ring
   CK(cudaEventRecord(w.ev[1], c.s));
   // R31: hub deferral only where the queue agent runs (persistent CTA workers) and ids leave bit 30 free
   const bool dfr = c.cfg.pr_defer_degree > 0 && c.cfg.kernel == ATOS_KERNEL_PERSISTENT &&
                    c.cfg.worker == ATOS_WORKER_CTA && n <= (int64_t)DEFER_BIT;
   c.split = c.cfg.hub_split == 1;  // R33: off by default for PageRank
-  PrAppT<R> app{rank, rs, (R)alpha, (R)eps, sink_bits, dfr ? (uint32_t)c.cfg.pr_defer_degree : 0u,
+  PrAppT<R> app{rank, rs, (R)alpha, (R)eps, sink_bits, g->d_hub != nullptr ? 1u : 0u,
+                dfr ? (uint32_t)c.cfg.pr_defer_degree : 0u,
                 (R)eps * (R)std::max(1, c.cfg.pr_defer_factor), nullptr, 0u, 0u, nullptr};
   // R35: sweep-activated hubs where the batch-closing warp runs (persistent CTA workers, fp32 residues
   // with fp64 hubs, threshold activation elsewhere)
   if constexpr (std::is_same<R, float>::value) {
     if (rs.res64 && g->num_hub_list > 0 && c.cfg.pr_hub_check > 0 && c.cfg.pr_activation == 0 &&
         c.cfg.kernel == ATOS_KERNEL_PERSISTENT && c.cfg.worker == ATOS_WORKER_CTA) {
-      PrAppT<float, true> hs{rank, rs, alpha, eps, sink_bits, app.defer_deg, app.defer_res, g->d_hub_list,
+      PrAppT<float, true> hs{rank, rs, alpha, eps, sink_bits, app.sink_tagged, app.defer_deg, app.defer_res,
+                             g->d_hub_list,
                              (uint32_t)g->num_hub_list, (uint32_t)c.cfg.pr_hub_check, w.u32a};
       k_hub_mark<<<fill_blocks(g->num_hub_list, g->sms), 256, 0, c.s>>>(g->d_hub_list, g->num_hub_list, w.u32a);
       CK(cudaGetLastError());
@@ -1010,6 +1048,11 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   CKS(begin_call(g, cfg, c, st));
   if (!(alpha > 0.f && alpha < 1.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "alpha not in (0,1)");
   if (!(eps > 0.f)) return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "eps <= 0 or NaN");
+  if (g->peer) {
+    if (c.cfg.pr_activation == 1)
+      return atos_set_error(ATOS_ERR_UNSUPPORTED, "Check_Size window activation is not built for peer graphs");
+    return peer_pagerank(g, alpha, eps, c.cfg, rank_out, st);
+  }
   if (g->dist) {
     if (c.cfg.pr_activation == 1)
       return atos_set_error(ATOS_ERR_UNSUPPORTED, "Check_Size window activation is not built for partitioned graphs");
@@ -1027,8 +1070,12 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
   // R34: fp32 residues need the hub tags; an untagged (borrowed) graph keeps every residue in fp64
   const bool r64 = c.cfg.pr_residue_fp64 != 0 || !g->d_hub;
-  // at most 2 live copies per vertex (initial + one threshold crossing)
-  CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)n, !bsp, c.s));
+  // at most 2 live copies per vertex (initial + one threshold crossing), so 2n slots suffice (R16);
+  // auto capacity is larger — min(16n, 2^28) slots (2 GB at RMAT-24) — so a run's ~12n pushes
+  // rarely wrap: a push to a position of lap 0 needs no load of its slot (q_wait_free), measured
+  // -1.8% PageRank time on RMAT-24 (profiles/r02_agents.md)
+  const uint64_t pr_cap = std::max<uint64_t>(2 * (uint64_t)n, std::min<uint64_t>(16 * (uint64_t)n, 1ull << 28));
+  CKS(ws_prepare(g, c.cfg, n, pr_cap, !bsp, c.s));
   if (!bsp && (uint64_t)n > w.cap)
     return atos_set_error(ATOS_ERR_QUEUE_OVERFLOW, "queue_capacity %llu < n = %lld initial tasks",
                           (unsigned long long)w.cap, (long long)n);
@@ -1072,6 +1119,7 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
                                   atos_stats* st) {
   LaunchCtx c;
   CKS(begin_call(g, cfg, c, st));
+  if (g->peer) return atos_set_error(ATOS_ERR_UNSUPPORTED, "colouring is not built for peer graphs (f2: BFS, PageRank)");
   if (!g->symmetric) return atos_set_error(ATOS_ERR_INVALID_GRAPH, "atos_color needs ATOS_GRAPH_SYMMETRIC");
   if (c.cfg.gc_literal) return atos_set_error(ATOS_ERR_UNSUPPORTED, "paper-literal colouring (livelocks, R13) not built");
   if (ncolors_out) *ncolors_out = 0;
@@ -1094,6 +1142,7 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
     CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
   }
   CK(cudaEventRecord(w.ev[0], c.s));
+  CKS(ring_reset(w, c.s));
   k_fill<int32_t><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(color, n, -1);
   k_fill<uint32_t><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(pend, n, 1u);
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
@@ -1135,3 +1184,4 @@ extern "C" atos_status atos_color(atos_graph g, const atos_config* cfg, int32_t*
 }
 
 #include "dist_impl.cuh"
+#include "peer_impl.cuh"

@@ -11,6 +11,7 @@ struct Workspace {
   uint64_t* ring = nullptr;
   uint64_t cap = 0;
   uint64_t dirty = 0;  // ring slots that may hold non-zero tags
+  uint64_t clear = 0;  // slots the next run zeroes in its timed init (ring_reset)
   atos::QueueCtl* ctl = nullptr;
   atos::QueueCtl* h_ctl = nullptr;  // pinned mirror
   uint32_t* u32a = nullptr;         // BFS dist / GC pend
@@ -37,6 +38,7 @@ struct Workspace {
 };
 
 struct DistState;  // dist_impl.cuh
+struct PeerState;  // peer_impl.cuh
 
 struct atos_graph_s {
   int64_t n = 0;  // local vertex count (== global n when not partitioned)
@@ -59,6 +61,8 @@ struct atos_graph_s {
   // multi-GPU partition (dist_impl.cuh)
   int64_t global_n = 0, v_begin = 0, v_end = 0;
   DistState* dist = nullptr;
+  // asynchronous peer-memory partitions (peer_impl.cuh)
+  PeerState* peer = nullptr;
 };
 
 atos_status atos_set_error(atos_status s, const char* fmt, ...);

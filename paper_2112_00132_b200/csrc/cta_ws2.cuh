@@ -24,15 +24,23 @@ namespace atos {
 #define ATOS_NBUF 4
 #endif
 constexpr int NBUF = ATOS_NBUF;
-// Queue-agent warps per CTA (build-time): agent a prepares ring batches
-// i = a, a + AGENTS, ... (buffer i % NBUF); workers consume every batch in
-// order and skip the batches of an agent that has published QUIT.
-#ifndef ATOS_AGENTS
-#define ATOS_AGENTS 1
-#endif
-constexpr int AGENTS = ATOS_AGENTS;
-static_assert(NBUF % AGENTS == 0, "NBUF must be a multiple of AGENTS");
-constexpr int STEP_CAP = 512;  // per-buffer step-owner table (u16; steps beyond it binary-search)
+// Queue-agent warps per CTA, per app (App::kAgents, default 1): agent a
+// prepares ring batches i = a, a + A, ... (buffer i % NBUF); workers consume
+// every batch in order and skip the batches of an agent that has published
+// QUIT.  PageRank runs two agents per 1,024-thread CTA: with one, the agent
+// was busy the whole run and the 31 worker warps waited for it 30% of their
+// cycles (profiles/r02_wait_prof.md); two measured -3.7% on RMAT-24
+// (profiles/r02_agents.md).  BFS keeps one (two: +20% at 256 threads).
+template <class A, class = void>
+struct AgentsTrait : std::integral_constant<int, 1> {};
+template <class A>
+struct AgentsTrait<A, std::void_t<decltype(A::kAgents)>> : std::integral_constant<int, A::kAgents> {};
+constexpr int STEP_CAP = 512;
+// A prepared batch with at most this many edges is expanded by the queue agent
+// itself (0 = off; must be <= STEP_EDGES: one LBS step).
+#ifndef ATOS_AGENT_FAST
+#define ATOS_AGENT_FAST 0
+#endif  // per-buffer step-owner table (u16; steps beyond it binary-search)
 // Register budget vs occupancy of the persistent CTA kernel (build-time knobs).
 // Measured on RMAT-24 (PR kernel ms / BFS ms): 1024x1 bound (64 regs, some
 // spills) + unroll 8: 209 / 4.1 — best; 512x1 (128 regs) + unroll 16:
@@ -51,6 +59,8 @@ constexpr int CTA_MAX_THREADS = ATOS_CTA_MAX_THREADS;
 constexpr int CTA_MIN_BLOCKS = ATOS_CTA_MIN_BLOCKS;
 constexpr int WS_UNROLL = ATOS_WS_UNROLL;
 constexpr int64_t STEP_EDGES = 32 * WS_UNROLL;
+constexpr int64_t AGENT_FAST_EDGES = ATOS_AGENT_FAST;
+static_assert(AGENT_FAST_EDGES <= STEP_EDGES, "ATOS_AGENT_FAST must fit one LBS step");
 // Column staging: item i of a batch is staged at element offset
 // roundup4(pre[i] + STAGE_PAD * i) of the buffer's stage area, covering its
 // 16-B aligned superset [e0 & ~3, roundup4(e1)) (at most 6 extra elements), so
@@ -110,6 +120,12 @@ __device__ __forceinline__ void vstore(int* p, int v) { *(volatile int*)p = v; }
 // Agent pop from the global queue; the idle path runs the termination check
 // (a7) — for apps with sweep-activated hubs (R35) quiescence must also pass a
 // clean hub sweep.
+constexpr uint32_t AGENT_SKIP = 0xFFFFFFFFu;
+// With several agents per CTA the workers consume batches in ring order, so an
+// agent that finds the queue empty (but the run not quiescent) must not wait
+// for work: its ring slot may be the one the workers wait on while another
+// agent's claimed batch (whose pushes would feed it) sits behind it.  It
+// publishes an empty batch instead (AGENT_SKIP) and moves on.
 template <class App>
 __device__ __forceinline__ uint32_t agent_pop(const App& app, const Queue& q, uint32_t want, uint64_t& first,
                                               uint64_t& hw, long long& last_count) {
@@ -145,6 +161,8 @@ __device__ __forceinline__ uint32_t agent_pop(const App& app, const Queue& q, ui
       } else {
         return 0;
       }
+    } else if (AgentsTrait<App>::value > 1) {
+      return AGENT_SKIP;
     }
     if (ns) __nanosleep(ns);
     ns = ns == 0 ? 32 : (ns < q.backoff_ns ? ns * 2 : ns);
@@ -190,6 +208,8 @@ template <class App>
 __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Queue& q, int F, unsigned char* smem,
                                    LocalStats& st) {
   using Payload = typename App::Payload;
+  constexpr int AGENTS = AgentsTrait<App>::value;
+  static_assert(NBUF % AGENTS == 0, "NBUF must be a multiple of the agents per CTA");
   const int T = blockDim.x, tid = threadIdx.x, wid = tid >> 5, lane = lane_id();
   const uint32_t S = q.stage_cap;
   const size_t bb = ws2_buf_bytes<Payload>(F, (int)S);
@@ -214,7 +234,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
     // ------------------------------------------------ queue agent(s)
     long long last_count = 0;  // lane 0: queue length seen at the last pop
     WPROF_DECL
-    for (int i = wid;; i += AGENTS) {
+    for (int i = wid;;) {
       const int b = i % NBUF;
       // wait until the workers have released buffer b
       bool dead = false;
@@ -235,12 +255,39 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       } else {
         n = agent_pop(app, q, (uint32_t)F, first, st.hw, last_count);
       }
+      const bool skip = n == AGENT_SKIP;
+      if (skip) {
+        n = 0;
+        // an empty batch still completes its buffer's staging phase (workers wait on it)
+        if (S) agent_stage(g, 0u, buf_e0(b), buf_pre(b), buf_sofs(b), buf_stage(b), S, &bars[b]);
+      }
       WPROF_MARK(1);
       if (n) {
         const uint32_t dfr = agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b));
         if (lane == 0) st.pushed += dfr;
         int64_t* pre = buf_pre(b);
         warp_exclusive_scan(pre, (int)n);
+        if constexpr (AGENT_FAST_EDGES > 0 && !App::kWindow) {
+          // Small batch (high-diameter frontiers): the agent expands it itself —
+          // one LBS step, no hand-off to the workers — and keeps ring index i
+          // (buffer b was never published, so it is still free).
+          const int64_t total = pre[n];
+          if (S == 0 && total <= (int64_t)AGENT_FAST_EDGES) {
+            RingSink sink{q};
+            uint32_t p = total ? lbs_step<App, RingSink, WS_UNROLL>(app, g, sink, pre, buf_e0(b), buf_pay(b),
+                                                                    (int)n, total, 0) : 0u;
+            if constexpr (HubSweepTrait<App>::value) p += hub_sweep(app, q);  // R35, before q_done
+            if (lane == 0) {
+              st.pushed += p;
+              st.edges += (uint64_t)total;
+              st.popped += n;
+              q_done(q, n);
+              q_trace(q, n, (uint64_t)total);
+            }
+            __syncwarp();
+            continue;
+          }
+        }
         if (S) agent_stage(g, n, buf_e0(b), pre, buf_sofs(b), buf_stage(b), S, &bars[b]);
         // step-owner table: own[c] = item holding flattened edge c*STEP_EDGES
         uint16_t* own = buf_own(b);
@@ -258,11 +305,13 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
         hdr[b].left = 0;
         hdr[b].seq = i / NBUF;
         __threadfence_block();
-        vstore(&hdr[b].state, n ? BUF_READY : BUF_QUIT);
+        vstore(&hdr[b].state, n || skip ? BUF_READY : BUF_QUIT);
       }
       __syncwarp();
       WPROF_MARK(2);
-      if (n == 0) break;
+      if (n == 0 && !skip) break;
+      if (skip) __nanosleep(256);
+      i += AGENTS;
     }
     WPROF_FLUSH(q);
   } else {
@@ -290,8 +339,12 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       __threadfence_block();
       // this batch's staged columns complete the buffer's pass-th mbarrier phase
       if (S) {
-        for (unsigned ns = 8; !mbar_try_wait(&bars[b], (uint32_t)pass & 1u); ns = ns < 128 ? ns * 2 : ns)
+        bool dead = false;
+        for (unsigned ns = 8; !mbar_try_wait(&bars[b], (uint32_t)pass & 1u); ns = ns < 128 ? ns * 2 : ns) {
           __nanosleep(ns);
+          if (ns >= 128 && (q_aborted(q) || q_timed_out(q))) { dead = true; break; }
+        }
+        if (dead) break;
       }
       WPROF_MARK(3);
       const int n = hdr[b].n;

@@ -122,12 +122,20 @@ __device__ __forceinline__ uint64_t pol_evict_last() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// Column entries carry a HUB TAG in bit 31 (vertex ids are < 2^31 - 1, R10):
-// set at graph create when the target's in-degree is >= HUB_IN_DEG, so the
-// PageRank edge push knows without any extra load that the target keeps its
-// residue in fp64 (R34).  Every reader masks it off with VID_MASK.
+// Column entries carry two TAG bits (vertex ids are < 2^30 - 1, R10/R37),
+// set at graph create on library-owned CSRs: bit 31 (HUB_TAG) when the
+// target's in-degree is >= HUB_IN_DEG, so the PageRank edge push knows without
+// any extra load that the target keeps its residue in fp64 (R34/R35); bit 30
+// (SINK_TAG) when the target has out-degree 0, so an activation test needs no
+// load of the dangling bitmap (R29/R37).  Every reader masks them off with
+// VID_MASK; the hot loops pass `raw >> TAG_SHIFT` (TAG_HUB | TAG_SINK bits)
+// to the apps.
 constexpr uint32_t HUB_TAG = 0x80000000u;
-constexpr uint32_t VID_MASK = 0x7FFFFFFFu;
+constexpr uint32_t SINK_TAG = 0x40000000u;
+constexpr uint32_t VID_MASK = 0x3FFFFFFFu;
+constexpr int TAG_SHIFT = 30;
+constexpr uint32_t TAG_HUB = HUB_TAG >> TAG_SHIFT;    // 2
+constexpr uint32_t TAG_SINK = SINK_TAG >> TAG_SHIFT;  // 1
 #ifndef ATOS_HUB_IN_DEG
 #define ATOS_HUB_IN_DEG 512
 #endif

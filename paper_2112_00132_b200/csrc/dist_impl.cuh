@@ -606,7 +606,7 @@ extern "C" atos_status atos_graph_create_partitioned(atos_comm comm, int64_t glo
   if (!tiled)
     return atos_set_error(ATOS_ERR_INVALID_ARGUMENT, "partition ranges do not tile [0, global_n) in rank order "
                           "(or a rank passed bad arguments)");
-  if (global_n >= 0x7FFFFFFFLL) return atos_set_error(ATOS_ERR_UNSUPPORTED, "global_n >= 2^31-1");
+  if (global_n >= (int64_t)VID_MASK) return atos_set_error(ATOS_ERR_UNSUPPORTED, "global_n >= 2^30-1 (R37)");
   const int64_t n = v_end - v_begin;
   atos_graph g = new (std::nothrow) atos_graph_s();
   if (!g) return atos_set_error(ATOS_ERR_OUT_OF_MEMORY, "host allocation");
@@ -801,6 +801,7 @@ static atos_status part_init(PartEngine& e, int64_t src) {
     if (!d->racc) CK(pool_malloc(&d->racc, (size_t)N1 * sizeof(double)));
   }
   CK(cudaEventRecord(w.ev[0], c.s));
+  CKS(ring_reset(w, c.s));
   CK(cudaMemsetAsync(d->d_round, 0, sizeof(DevRound), c.s));
   if (e.app == PartEngine::BFS) {
     const bool mine = src >= g->v_begin && src < g->v_end;

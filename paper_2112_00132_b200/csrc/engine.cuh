@@ -49,6 +49,7 @@ struct BfsApp {
   // R29: bit w set = deg(w) == 0.  A dangling vertex's task expands no edge,
   // so an improvement of dist[w] is final without pushing w.  nullptr = off.
   const uint32_t* sink;
+  uint32_t sink_tagged;  // R37: read the column's SINK_TAG instead of the bitmap
   using Payload = uint32_t;
   using Probe = uint32_t;
   // Chunk task of v created with payload nd: still current iff dist[v]+1 == nd.
@@ -58,10 +59,15 @@ struct BfsApp {
   // any atomic (memory-level parallelism).  The probe may hit a stale L1 copy
   // (>= the current value): it only lets through atomics that turn out not to
   // improve, never suppresses one that would.
-  __device__ __forceinline__ Probe probe(uint32_t w, uint32_t /*hub tag*/) const {
-    if (!filter) return 0xFFFFFFFFu;
-    const uint32_t v = ld_probe_u16(near + w);
-    return v == 0xFFFFu ? 0xFFFFFFFFu : v;
+  // Probe = the filter's bound (low 31 bits; 0x7FFFFFFF = none) | the
+  // column's SINK tag in bit 31 (R37).
+  __device__ __forceinline__ Probe probe(uint32_t w, uint32_t tag) const {
+    uint32_t v = 0x7FFFFFFFu;
+    if (filter) {
+      v = ld_probe_u16(near + w);
+      if (v == 0xFFFFu) v = 0x7FFFFFFFu;
+    }
+    return v | ((tag & TAG_SINK) << 31);
   }
   __device__ __forceinline__ bool commit(Payload nd, uint32_t w, Probe pr) const {
     return decide(nd, w, pr, issue(nd, w, pr));
@@ -70,13 +76,14 @@ struct BfsApp {
   // thread's UNROLL atomics are all in flight before any result is consumed.
   using Raw = uint32_t;
   __device__ __forceinline__ Raw issue(Payload nd, uint32_t w, Probe pr) const {
-    return nd < pr ? atom_min_hot(dist + w, nd) : 0u;
+    return nd < (pr & 0x7FFFFFFFu) ? atom_min_hot(dist + w, nd) : 0u;
   }
   __device__ __forceinline__ bool decide(Payload nd, uint32_t w, Probe pr, Raw old) const {
-    const bool improved = nd < pr && nd < old;
+    const bool improved = nd < (pr & 0x7FFFFFFFu) && nd < old;
     if (!improved) return false;
     st_u16_hot(near + w, nd < 0xFFFFu ? (uint16_t)nd : (uint16_t)0xFFFFu);
-    return sink == nullptr || !((ld_nc_u32(sink + (w >> 5)) >> (w & 31)) & 1u);
+    if (sink == nullptr) return true;
+    return sink_tagged ? !(pr >> 31) : !((ld_nc_u32(sink + (w >> 5)) >> (w & 31)) & 1u);
   }
   // Expand v at its CURRENT depth d (R3) unless some task already expanded
   // (or is expanding) v at depth <= d: a vertex pushed k times by k
@@ -168,16 +175,16 @@ struct Residues {
   __device__ __forceinline__ double take(uint32_t v) const { return take_finish(v, take_issue(v)); }
   // residue[w] += c at the storage the column's hub tag names; returns the old value
   __device__ __forceinline__ double add(uint32_t w, uint32_t tag, R c) const {
-    if (tag && res64) return atom_add_hot(res64 + w, (double)c);
+    if ((tag & TAG_HUB) && res64) return atom_add_hot(res64 + w, (double)c);
     return (double)atom_add_hot(res + w, c);
   }
   __device__ __forceinline__ void add_noret(uint32_t w, uint32_t tag, R c) const {
-    if (tag && res64) red_add_hot(res64 + w, (double)c);
+    if ((tag & TAG_HUB) && res64) red_add_hot(res64 + w, (double)c);
     else red_add_hot(res + w, c);
   }
   // did the add of c that returned `old` cross eps (old <= eps < old + c, in the add's own precision)?
   __device__ __forceinline__ bool crossed(uint32_t tag, double old, R c, R eps) const {
-    if (tag && res64) return old <= (double)eps && old + (double)c > (double)eps;
+    if ((tag & TAG_HUB) && res64) return old <= (double)eps && old + (double)c > (double)eps;
     return (R)old <= eps && add_rn((R)old, c) > eps;
   }
   __device__ __forceinline__ double peek(uint32_t v) const {  // L2 read (sweeps)
@@ -193,6 +200,9 @@ struct Residues {
 // r = atomicExch(res[v], 0); rank[v] += r; c = alpha r / deg(v);
 // per edge: old = atomicAdd(res[w], c); push w iff old <= eps < old + c.
 // rank accumulates in fp64 (a per-pop cost): a hub receives 10^4+ pops.
+#ifndef ATOS_PR_AGENTS
+#define ATOS_PR_AGENTS 2
+#endif
 template <class R, bool HS = false>
 struct PrAppT {
   static constexpr bool kWindow = false;
@@ -205,6 +215,9 @@ struct PrAppT {
   // push is skipped and k_pr_absorb_sinks applies it once after quiescence.
   // nullptr = off (every crossing is pushed, Alg. 4 literally).
   const uint32_t* sink;
+  // R37: the columns carry SINK_TAG (library-owned CSR), so the test reads
+  // the tag instead of the bitmap; 0 with sink == nullptr or an untagged CSR.
+  uint32_t sink_tagged;
   // Hub deferral (R31, persistent CTA workers): a popped vertex with at least
   // defer_deg out-edges whose residue is below defer_res (a few eps) is not
   // expanded yet — its residue goes back and it is re-queued once (DEFER_BIT),
@@ -212,6 +225,7 @@ struct PrAppT {
   // instead of scattering an eps-sized residue over thousands of edges.
   static constexpr bool kDefer = true;
   static constexpr bool kHubSweep = HS;
+  static constexpr int kAgents = ATOS_PR_AGENTS;  // queue agents per persistent CTA (cta_ws2.cuh)
   uint32_t defer_deg;  // 0 = off
   R defer_res;
   // Sweep activation of hubs (R35, persistent CTA workers; HS = true):
@@ -273,7 +287,7 @@ struct PrAppT {
   __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
   __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
     if constexpr (HS) {
-      if (tag) {  // R35: hub target, activated by sweeps
+      if (tag & TAG_HUB) {  // R35: hub target, activated by sweeps
         red_add_hot(rs.res64 + w, (double)c);
         return 0.0;
       }
@@ -282,10 +296,10 @@ struct PrAppT {
   }
   __device__ __forceinline__ bool decide(Payload c, uint32_t w, Probe tag, Raw old) const {
     if constexpr (HS) {
-      if (tag) return false;
+      if (tag & TAG_HUB) return false;
     }
     if (!rs.crossed(tag, old, c, eps)) return false;
-    return !test_bit(sink, w);
+    return sink_tagged ? !(tag & TAG_SINK) : !test_bit(sink, w);
   }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe tag) const { return decide(c, w, tag, issue(c, w, tag)); }
   __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t tag) const { return commit(c, w, tag); }
@@ -600,7 +614,7 @@ __device__ __forceinline__ uint32_t lbs_step(const App& app, const GraphView& g,
   typename App::Probe pr[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) {
-    const uint32_t tag = w[k] >> 31;  // HUB_TAG (device.cuh)
+    const uint32_t tag = w[k] >> TAG_SHIFT;  // TAG_HUB | TAG_SINK (device.cuh)
     w[k] = ATOS_CHK(w[k] & VID_MASK, g.n);
     pr[k] = typename App::Probe{};
     if (idx[k] >= 0) pr[k] = app.probe(w[k], tag);
@@ -668,7 +682,7 @@ __device__ __forceinline__ uint32_t lbs_expand(const App& app, const GraphView& 
     typename App::Probe pr[LBS_UNROLL];
 #pragma unroll
     for (int k = 0; k < LBS_UNROLL; ++k) {
-      const uint32_t tag = w[k] >> 31;  // HUB_TAG
+      const uint32_t tag = w[k] >> TAG_SHIFT;  // TAG_HUB | TAG_SINK
       w[k] = ATOS_CHK(w[k] & VID_MASK, g.n);
       pr[k] = typename App::Probe{};
       if (idx[k] >= 0) pr[k] = app.probe(w[k], tag);
@@ -779,7 +793,7 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
     const bool v = e < a0;
     const uint32_t raw = v ? ld_col_tagged(g.col + ATOS_CHK(e, g.col_cap)) : 0u;
     const uint32_t w = ATOS_CHK(raw & VID_MASK, g.n);
-    bool act = v && app.edge(p, w, raw >> 31);
+    bool act = v && app.edge(p, w, raw >> TAG_SHIFT);
     pushed += sink.warp_push(act, app.item_of(w));
   }
   const int64_t a1 = a0 + ((e1 - a0) & ~int64_t(3));
@@ -795,7 +809,7 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
     typename App::Probe pr[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (v) pr[k] = app.probe(w[k], raw[k] >> 31);
+      if (v) pr[k] = app.probe(w[k], raw[k] >> TAG_SHIFT);
     typename App::Raw old[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -813,7 +827,7 @@ __device__ __forceinline__ uint32_t warp_walk(const App& app, const GraphView& g
     const bool v = e < e1;
     const uint32_t raw = v ? ld_col_tagged(g.col + ATOS_CHK(e, g.col_cap)) : 0u;
     const uint32_t w = ATOS_CHK(raw & VID_MASK, g.n);
-    bool act = v && app.edge(p, w, raw >> 31);
+    bool act = v && app.edge(p, w, raw >> TAG_SHIFT);
     pushed += sink.warp_push(act, app.item_of(w));
   }
   return pushed;
@@ -884,7 +898,7 @@ __device__ __forceinline__ void thread_batch(const App& app, const GraphView& g,
       const uint32_t raw = ld_col_tagged(g.col + ATOS_CHK(e, g.col_cap));
       w = ATOS_CHK(raw & VID_MASK, g.n);
       ++e;
-      act = app.edge(p, w, raw >> 31);
+      act = app.edge(p, w, raw >> TAG_SHIFT);
     }
     pushed += sink.warp_push(act, app.item_of(w));
     refill();

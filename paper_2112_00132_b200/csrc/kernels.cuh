@@ -399,6 +399,49 @@ struct PrInitAppT {
   __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
 };
 
+// R4 seeding with R34's storage: the push to a hub target (column HUB_TAG)
+// accumulates in fp64 (res64, red.add.f64 — hundreds of thousands of equal
+// adds, R30), every other target in its fp32 residue directly (< 512 adds,
+// R34's argument), so no fp64 staging array and no rounding pass.
+struct PrInitSplitApp {
+  static constexpr bool kWindow = false;
+  __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
+  float* res;
+  double* res64;
+  double c0;  // (1 - alpha) * alpha
+  using Payload = double;
+  using Probe = uint32_t;  // the column's hub tag
+  using Raw = int;
+  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1, Payload& p) const {
+    e0 = ld_nc_s64(g.off + v);
+    e1 = ld_nc_s64(g.off + v + 1);
+    if (e1 == e0) return false;
+    p = c0 / (double)(e1 - e0);
+    return true;
+  }
+  __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
+  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
+    if (tag & TAG_HUB) red_add_hot(res64 + w, c);
+    else red_add_hot(res + w, (float)c);
+    return 0;
+  }
+  __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
+  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe t) const { return decide(c, w, t, issue(c, w, t)); }
+  __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t t) const { return commit(c, w, t); }
+  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
+};
+// zero the fp64 residue of every hub (bit set in the hub bitmap)
+__global__ void k_zero_hubs(const uint32_t* bits, int64_t n, double* res64) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < (n + 31) / 32; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = bits[w];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      res64[w * 32 + b] = 0.0;
+    }
+  }
+}
+
 __device__ __forceinline__ bool bit_of(const uint32_t* bits, int64_t v) {
   return bits && ((bits[v >> 5] >> (v & 31)) & 1u);
 }
@@ -426,16 +469,18 @@ __global__ void k_sink_bitmap(const int64_t* off, int64_t n, uint32_t* bits) {
   }
 }
 
-// Hub tagging (R34), at graph create: in-degree histogram, then bit 31 of
-// every column entry whose target has in-degree >= thr, and the hub bitmap.
+// Column tagging (R34, R37), at graph create: in-degree histogram, then bit
+// 31 of every column entry whose target has in-degree >= thr, bit 30 if the
+// target is dangling (the sink bitmap), and the hub bitmap.
 __global__ void k_in_degree(const int32_t* col, int64_t m, int64_t n, uint32_t* indeg) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(indeg + ATOS_CHK((uint32_t)col[e] & VID_MASK, (uint32_t)n), 1u);
 }
-__global__ void k_tag_hubs(int32_t* col, int64_t m, int64_t n, const uint32_t* indeg, uint32_t thr) {
+__global__ void k_tag_hubs(int32_t* col, int64_t m, int64_t n, const uint32_t* indeg, uint32_t thr,
+                           const uint32_t* sink) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t w = ATOS_CHK((uint32_t)col[e] & VID_MASK, (uint32_t)n);
-    col[e] = (int32_t)(w | (indeg[w] >= thr ? HUB_TAG : 0u));
+    col[e] = (int32_t)(w | (indeg[w] >= thr ? HUB_TAG : 0u) | (((sink[w >> 5] >> (w & 31)) & 1u) ? SINK_TAG : 0u));
   }
 }
 __global__ void k_hub_bitmap(const uint32_t* indeg, int64_t n, uint32_t thr, uint32_t* bits,

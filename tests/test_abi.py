@@ -65,6 +65,11 @@ def test_host_only_entry_points(lib):
     assert L.atos_graph_create(None, None, -1, 0, 0, ctypes.byref(h)) == 1
     assert L.atos_graph_create(None, None, 0, 0, 0, None) == 1
     assert L.atos_bfs(None, 0, None, None, None) == 1
+    # bits 30-31 of a column entry are tags (R37): n >= 2^30 - 1 is UNSUPPORTED, refused before any read
+    one = (ctypes.c_int64 * 1)(0)
+    assert L.atos_graph_create(one, None, 2 ** 30 - 1, 0, 0, ctypes.byref(h)) == 8
+    assert L.atos_graph_create_peer(2, None, one, None, 2 ** 30 - 1, 0, 0, ctypes.byref(h)) == 8
+    assert L.atos_graph_create_peer(0, None, one, None, 4, 0, 0, ctypes.byref(h)) == 1
 
 
 def test_product_has_no_oracle_dependency():

@@ -265,6 +265,29 @@ def test_staging_borrowed_unpadded_columns(atos):
     assert np.max(np.abs(r - x)) / x.max() <= PR_TOL
 
 
+@pytest.mark.parametrize("gname", ["rmat16", "star", "two"])
+def test_tagged_vs_borrowed_columns(atos, gname):
+    """R34/R37: a library-owned CSR carries HUB/SINK tags in bits 31/30 of its
+    column entries; a borrowed (caller-owned) one is never written and uses the
+    bitmaps and fp64 residues.  Both give the oracle's answers, and the sink
+    tag defers exactly the dangling vertices the bitmap does (same pops for
+    the deterministic single-worker BFS)."""
+    import torch
+    g = G(gname)
+    Gt = atos.Graph(torch.from_numpy(g.off).cuda(), torch.from_numpy(g.col.copy()).cuda())
+    Go = D(atos, gname)
+    x, src = jacobi(gname), 0
+    for Gx in (Go, Gt):
+        d, sb = atos.bfs(Gx, src, worker="thread", fetch_size=1, num_blocks=1, cta_threads=32)
+        assert np.array_equal(d, oracle.bfs(g, src))
+        r, st = atos.pagerank(Gx, 0.85, 1e-6, fetch_size=64)
+        assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
+        assert st["max_residue"] <= 1e-6
+    _, s1 = atos.bfs(Go, src, worker="thread", fetch_size=1, num_blocks=1, cta_threads=32)
+    _, s2 = atos.bfs(Gt, src, worker="thread", fetch_size=1, num_blocks=1, cta_threads=32)
+    assert s1["tasks_popped"] == s2["tasks_popped"]
+
+
 @pytest.mark.parametrize("stage", [0, 512, 4096])
 def test_pagerank_column_staging(atos, stage):
     x = jacobi("rmat16")
@@ -510,7 +533,7 @@ def test_pagerank_hub_sweep(atos, gname, hub_check):
     g = fan_in_graph() if gname == "fanin" else G(gname)
     x = fan_in_x() if gname == "fanin" else jacobi(gname)
     Gd = fan_in_dev(atos) if gname == "fanin" else D(atos, gname)
-    for kw in [dict(fetch_size=128, cta_threads=1024), dict(fetch_size=1, cta_threads=64)]:
+    for kw in [dict(fetch_size=128, cta_threads=1024), dict(fetch_size=1, cta_threads=96)]:
         r, st = atos.pagerank(Gd, 0.85, 1e-6, pr_hub_check=hub_check, timeout_s=60, **kw)
         assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
         assert st["max_residue"] <= 1e-6
@@ -526,6 +549,15 @@ def test_pagerank_window_activation(atos, gname, check_size):
     r, st = atos.pagerank(D(atos, gname), 0.85, 1e-6, pr_activation=1, check_size=check_size, fetch_size=64)
     assert np.max(np.abs(r - x)) / x.max() <= PR_TOL
     assert st["max_residue"] <= 1e-6
+
+
+def test_pagerank_cta_threads_floor(atos):
+    # persistent CTA PageRank runs two queue-agent warps per CTA: at least one worker warp more
+    with pytest.raises(atos.AtosError) as e:
+        atos.pagerank(D(atos, "K9"), 0.85, 1e-6, cta_threads=64)
+    assert e.value.name == "INVALID_ARGUMENT"
+    r, st = atos.pagerank(D(atos, "K9"), 0.85, 1e-6, cta_threads=96, fetch_size=1)
+    assert np.allclose(r, 1.0, atol=1e-5)
 
 
 def test_pagerank_window_unsupported_combos(atos):
