@@ -299,6 +299,7 @@ struct PrAppT {
       if (tag & TAG_HUB) return false;
     }
     if (!rs.crossed(tag, old, c, eps)) return false;
+    if (sink == nullptr) return true;  // sink deferral off: push every crossing
     return sink_tagged ? !(tag & TAG_SINK) : !test_bit(sink, w);
   }
   __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe tag) const { return decide(c, w, tag, issue(c, w, tag)); }

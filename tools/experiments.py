@@ -50,28 +50,53 @@ def heatmap():
 
 
 def kernels():
+    """Persistent vs discrete vs BSP for the three apps (configs[2]; the paper's strategy comparison,
+    P:1025-1027) in the bench configuration, with the work of each schedule relative to BSP's (the
+    tbl:extrawork overwork lens): BFS pops / BSP pops, PageRank edge pushes / BSP edge
+    pushes, colouring tasks / 2n."""
     g = gg.rmat(24, 16, seed=1)
     G = atos.Graph.from_csr(g)
     deg = g.degrees()
-    print("\n### RMAT-24: persistent vs discrete vs BSP (CTA workers)\n")
-    print("| app | kernel | ms | launches | rounds | pops | edges | GTEPS |")
-    print("|---|---|---|---|---|---|---|---|")
+    print("\n### RMAT-24: persistent vs discrete vs BSP (CTA workers, bench configuration)\n")
+    print("| app | kernel | ms | launches | rounds | pops | edges | work / BSP | GTEPS |")
+    print("|---|---|---|---|---|---|---|---|---|")
+    rows = []
     for kern, dl in [("persistent", False), ("discrete", False), ("discrete", True), ("bsp", False)]:
-        (d, st), ms = timed(lambda: atos.bfs(G, 0, kernel=kern, device_loop=dl, fetch_size=128, timeout_s=300), 3)
-        e = int(deg[d != atos.UNREACHED].sum())
-        name = kern + (" (device loop)" if dl else "")
-        print(f"| BFS | {name} | {ms:.2f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
-              f"{st['edges_processed']} | {e / ms / 1e6:.1f} |", flush=True)
+        (d, st), ms = timed(lambda: atos.bfs(G, 0, kernel=kern, device_loop=dl, fetch_size=128, cta_threads=256,
+                                             timeout_s=300), 3)
+        rows.append(("BFS", kern + (" (device loop)" if dl else ""), ms, st, int(deg[d != atos.UNREACHED].sum())))
+    bsp_pops = rows[-1][3]["tasks_popped"]
+    for app, name, ms, st, e in rows:
+        print(f"| {app} | {name} | {ms:.2f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
+              f"{st['edges_processed']} | {st['tasks_popped'] / bsp_pops:.3f} (pops) | {e / ms / 1e6:.1f} |", flush=True)
+    rows = []
     for kern, dl in [("persistent", False), ("discrete", False), ("discrete", True), ("bsp", False)]:
         (r, st), ms = timed(lambda: atos.pagerank(G, 0.85, 1e-6, kernel=kern, device_loop=dl, fetch_size=128,
-                                                  cta_threads=512, timeout_s=300), 1)
-        name = kern + (" (device loop)" if dl else "")
-        print(f"| PageRank | {name} | {ms:.1f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
-              f"{st['edges_processed']} | {st['edges_processed'] / ms / 1e6:.1f} (raw) |", flush=True)
+                                                  cta_threads=1024 if kern == "persistent" else 256,
+                                                  timeout_s=300), 2)
+        rows.append(("PageRank", kern + (" (device loop)" if dl else ""), ms, st))
     (r, st), ms = timed(lambda: atos.pagerank(G, 0.85, 1e-6, pr_activation=1, check_size=8, fetch_size=128,
                                               cta_threads=512, timeout_s=300), 1)
-    print(f"| PageRank (Check_Size=8 window, f1) | persistent | {ms:.1f} | {st['kernel_launches']} | {st['rounds']} | "
-          f"{st['tasks_popped']} | {st['edges_processed']} | {st['edges_processed'] / ms / 1e6:.1f} (raw) |", flush=True)
+    rows.append(("PageRank (Check_Size=8 window, f1)", "persistent", ms, st))
+    bsp_e = rows[3][3]["edges_processed"]
+    for app, name, ms, st in rows:
+        print(f"| {app} | {name} | {ms:.1f} | {st['kernel_launches']} | {st['rounds']} | {st['tasks_popped']} | "
+              f"{st['edges_processed']} | {st['edges_processed'] / bsp_e:.3f} (edge pushes) | "
+              f"{bsp_e / ms / 1e6:.1f} (norm) |", flush=True)
+    s = gg.rmat(22, 16, seed=1, symmetrize=True)
+    S = atos.Graph.from_csr(s, symmetric=True)
+    for kern, w, f in [("persistent", "cta", 128), ("persistent", "warp", 128), ("discrete", "warp", 32),
+                       ("discrete", "cta", 32), ("bsp", "warp", 32), ("bsp", "cta", 32)]:
+        (c, k, st), ms = timed3(lambda: atos.color(S, kernel=kern, worker=w, fetch_size=f, cta_threads=256,
+                                                   timeout_s=300), 2)
+        print(f"| colouring RMAT-22 sym ({k} colours) | {kern} {w} F={f} | {ms:.1f} | {st['kernel_launches']} | "
+              f"{st['rounds']} | {st['tasks_popped']} | {st['edges_processed']} | "
+              f"{st['tasks_popped'] / (2 * s.n):.3f} (tasks / 2n) | - |", flush=True)
+
+
+def timed3(fn, reps=3):
+    out = [fn() for _ in range(reps)]
+    return out[-1], statistics.median(o[-1]["ms"] for o in out)
 
 
 def color():
@@ -119,22 +144,30 @@ def grid():
 
 
 def timeline():
+    """Cumulative work vs time (the paper's throughput-over-time figures) for the three apps
+    in the bench configuration; colouring on the symmetrised RMAT-22."""
     g = gg.rmat(24, 16, seed=1)
     G = atos.Graph.from_csr(g)
-    tr = atos.Trace(1 << 22)
-    for app in ["bfs", "pr"]:
+    s = gg.rmat(22, 16, seed=1, symmetrize=True)
+    S = atos.Graph.from_csr(s, symmetric=True)
+    tr = atos.Trace(1 << 23)
+    for app in ["bfs", "pr", "color"]:
         if app == "bfs":
             atos.bfs(G, 0, fetch_size=128)
             _, st = atos.bfs(G, 0, fetch_size=128, trace=tr)
+        elif app == "pr":
+            _, st = atos.pagerank(G, 0.85, 1e-6, fetch_size=128, cta_threads=1024, trace=tr)
         else:
-            _, st = atos.pagerank(G, 0.85, 1e-6, fetch_size=128, cta_threads=512, trace=tr)
+            atos.color(S, fetch_size=128)
+            _, _, st = atos.color(S, fetch_size=128, trace=tr)
         r = tr.records(st)
         t = (r["t_ns"] - r["t_ns"][0]) / 1e3
         nb = 20
         edges = np.linspace(0, t[-1] + 1e-9, nb + 1)
         idx = np.clip(np.searchsorted(edges, t, side="right") - 1, 0, nb - 1)
         tot = r["edges"].astype(np.int64).sum()
-        print(f"\n### Timeline: {app.upper()} RMAT-24 ({st['ms']:.2f} ms, {len(r)} batches)\n")
+        gname = "RMAT-22 symmetrised" if app == "color" else "RMAT-24"
+        print(f"\n### Timeline: {app.upper()} {gname} ({st['ms']:.2f} ms, {len(r)} batches)\n")
         print("| t (us) | batches | items | edges | cum. edges % | SMs active |")
         print("|---|---|---|---|---|---|")
         cum = 0
