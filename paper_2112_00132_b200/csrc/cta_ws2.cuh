@@ -126,7 +126,7 @@ constexpr uint32_t AGENT_SKIP = 0xFFFFFFFFu;
 // for work: its ring slot may be the one the workers wait on while another
 // agent's claimed batch (whose pushes would feed it) sits behind it.  It
 // publishes an empty batch instead (AGENT_SKIP) and moves on.
-template <class App>
+template <class App, bool kSkip = true>
 __device__ __forceinline__ uint32_t agent_pop(const App& app, const Queue& q, uint32_t want, uint64_t& first,
                                               uint64_t& hw, long long& last_count) {
   const int lane = lane_id();
@@ -161,7 +161,7 @@ __device__ __forceinline__ uint32_t agent_pop(const App& app, const Queue& q, ui
       } else {
         return 0;
       }
-    } else if (AgentsTrait<App>::value > 1) {
+    } else if (kSkip && AgentsTrait<App>::value > 1) {
       return AGENT_SKIP;
     }
     if (ns) __nanosleep(ns);
