@@ -44,6 +44,9 @@ struct GcApp {
 enum GcMode : int { GC_UBER = 0, GC_BSP_ASSIGN = 1, GC_BSP_DETECT = 2 };
 
 constexpr int GC_WIN_WORDS = 8;  // 256-colour window per pass (CTA and warp workers)
+#ifndef ATOS_GC_WIN_MAX
+#define ATOS_GC_WIN_MAX 1024  // largest per-item window of a short CTA batch, in words
+#endif
 
 // ------------------------------------------------------------ CTA worker ---
 struct GcCtaSmem {
@@ -51,7 +54,8 @@ struct GcCtaSmem {
   int64_t* pre;    // [F+1]
   uint32_t* task;  // [F] task word; 0xFFFFFFFF = done/empty
   int32_t* col_v;  // [F] CHECK: colour of v ; ASSIGN: window base
-  uint32_t* bits;  // [F * GC_WIN_WORDS] ASSIGN forbidden window
+  uint32_t* bits;  // [F * GC_WIN_WORDS] ASSIGN forbidden windows, ww words per item of a batch
+  int win_total;   // F * GC_WIN_WORDS
   int32_t* flag;   // [F] CHECK: self-conflict flag ; ASSIGN: needs another pass
   int64_t* wsum;   // [32]
   int32_t* cnt;    // [2]
@@ -71,20 +75,29 @@ __device__ __forceinline__ GcCtaSmem gc_smem_carve(unsigned char* base, int F) {
   s.flag = s.col_v + F;
   s.bits = reinterpret_cast<uint32_t*>(s.flag + F);
   s.cnt = reinterpret_cast<int32_t*>(s.bits + (size_t)F * GC_WIN_WORDS);
+  s.win_total = F * GC_WIN_WORDS;
   return s;
 }
 
-__device__ __forceinline__ int gc_first_free(const uint32_t* w) {
-#pragma unroll
-  for (int k = 0; k < GC_WIN_WORDS; ++k)
+__device__ __forceinline__ int gc_first_free(const uint32_t* w, int words = GC_WIN_WORDS) {
+  for (int k = 0; k < words; ++k)
     if (w[k] != 0xFFFFFFFFu) return k * 32 + __ffs(~w[k]) - 1;
   return -1;
+}
+// Colour-window words per item of a CTA batch of n tasks: the batch's whole
+// bitmap area is shared out, so a short batch — typically one hub task in a
+// run's tail — scans its neighbours' colours in one pass instead of one pass
+// per 256 colours (a hub of RMAT-24 sees ~870 colours).
+__device__ __forceinline__ int gc_window_words(int win_total, uint32_t n) {
+  const int w = n ? win_total / (int)n : win_total;
+  return max(GC_WIN_WORDS, min(ATOS_GC_WIN_MAX, w));
 }
 
 template <int MODE, class Src, class Sink>
 __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& src, const Sink& sink, uint32_t n,
                              GcCtaSmem& sm, LocalStats& st) {
   const int T = blockDim.x, tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const int ww = gc_window_words(sm.win_total, n);
   // phase 1: read tasks
   bool fenced = false;
   for (int i = tid; i < (int)n; i += T) {
@@ -103,7 +116,7 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
         if (MODE == GC_UBER) { atomicExch(app.pend + v, 0u); fenced = true; }
         sm.col_v[i] = 0;  // window base
 #pragma unroll
-        for (int k = 0; k < GC_WIN_WORDS; ++k) sm.bits[i * GC_WIN_WORDS + k] = 0;
+        for (int k = 0; k < ww; ++k) sm.bits[i * ww + k] = 0;
       }
     } else {
       sm.e0[i] = 0;
@@ -143,7 +156,7 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
             }
           } else {
             const int32_t r = cu - sm.col_v[i];
-            if (r >= 0 && r < 32 * GC_WIN_WORDS) atomicOr(sm.bits + i * GC_WIN_WORDS + (r >> 5), 1u << (r & 31));
+            if (r >= 0 && r < 32 * ww) atomicOr(sm.bits + i * ww + (r >> 5), 1u << (r & 31));
           }
         }
       }
@@ -159,7 +172,7 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
       const uint32_t t = sm.task[i];
       int64_t deg = 0;
       if (t != 0xFFFFFFFFu && !(t & GC_CHECK_BIT)) {
-        const int f = gc_first_free(sm.bits + i * GC_WIN_WORDS);
+        const int f = gc_first_free(sm.bits + i * ww, ww);
         const uint32_t v = t;
         if (f >= 0) {
           st_relaxed_s32(app.color + app.vb + v, sm.col_v[i] + f);
@@ -167,9 +180,8 @@ __device__ void gc_cta_batch(const GcApp& app, const GraphView& g, const Src& sr
           stored = true;
           sm.flag[i] = 2;  // assigned in this batch
         } else {
-          sm.col_v[i] += 32 * GC_WIN_WORDS;
-#pragma unroll
-          for (int k = 0; k < GC_WIN_WORDS; ++k) sm.bits[i * GC_WIN_WORDS + k] = 0;
+          sm.col_v[i] += 32 * ww;
+          for (int k = 0; k < ww; ++k) sm.bits[i * ww + k] = 0;
           deg = ld_nc_s64(g.off + v + 1) - sm.e0[i];
           again = 1;
         }
