@@ -121,9 +121,6 @@ __device__ __forceinline__ void vstore(int* p, int v) { *(volatile int*)p = v; }
 // (a7) — for apps with sweep-activated hubs (R35) quiescence must also pass a
 // clean hub sweep.
 constexpr uint32_t AGENT_SKIP = 0xFFFFFFFFu;
-#ifndef ATOS_EARLY_RESV
-#define ATOS_EARLY_RESV 1
-#endif
 // With several agents per CTA the workers consume batches in ring order, so an
 // agent that finds the queue empty (but the run not quiescent) must not wait
 // for work: its ring slot may be the one the workers wait on while another
@@ -236,13 +233,6 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
   if (wid < AGENTS) {
     // ------------------------------------------------ queue agent(s)
     long long last_count = 0;  // lane 0: queue length seen at the last pop
-    // Early reservation: while the queue is long, the agent issues the `count`
-    // fetch-and-add of its NEXT pop right after preparing a batch and consumes
-    // the result one iteration later, so that atomic's L2 round trip overlaps
-    // the scan, the hand-off and the wait for a free buffer instead of sitting
-    // on the pop's critical path (q_try_pop's protocol, split in two).
-    long long resv_old = 0;  // lane 0
-    uint32_t resv_want = 0;  // warp-uniform
     WPROF_DECL
     for (int i = wid;;) {
       const int b = i % NBUF;
@@ -263,25 +253,7 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       if constexpr (App::kWindow) {
         n = window_pop(app, q, (uint32_t)F, first, st.hw);
       } else {
-        if (ATOS_EARLY_RESV && resv_want) {
-          uint32_t rn = 0;
-          if (lane == 0) {
-            const long long old = resv_old;
-            rn = old >= (long long)resv_want ? resv_want : (old > 0 ? (uint32_t)old : 0u);
-            if (rn < resv_want)  // return what was not published
-              atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->count.v),
-                        (unsigned long long)(long long)(resv_want - rn));
-            if (rn) {
-              first = atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->head.v), (unsigned long long)rn);
-              if ((uint64_t)old > st.hw) st.hw = (uint64_t)old;
-              last_count = old - (long long)rn;
-            }
-          }
-          resv_want = 0;
-          n = __shfl_sync(FULL_MASK, rn, 0);
-          first = __shfl_sync(FULL_MASK, first, 0);
-        }
-        if (n == 0) n = agent_pop(app, q, (uint32_t)F, first, st.hw, last_count);
+        n = agent_pop(app, q, (uint32_t)F, first, st.hw, last_count);
       }
       const bool skip = n == AGENT_SKIP;
       if (skip) {
@@ -293,18 +265,6 @@ __device__ void cta_ws2_persistent(const App& app, const GraphView& g, const Que
       if (n) {
         const uint32_t dfr = agent_prepare(app, g, q, cq, first, n, buf_e0(b), buf_pre(b), buf_pay(b));
         if (lane == 0) st.pushed += dfr;
-        if constexpr (!App::kWindow) {
-          if (ATOS_EARLY_RESV) {
-            uint32_t w = 0;
-            if (lane == 0 && last_count > 8ll * F) {
-              w = (uint32_t)F;
-              if (q.workers) w = (uint32_t)min((long long)w, (last_count + q.workers - 1) / q.workers);
-              resv_old = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&q.ctl->count.v),
-                                              (unsigned long long)(-(long long)w));
-            }
-            resv_want = __shfl_sync(FULL_MASK, w, 0);
-          }
-        }
         int64_t* pre = buf_pre(b);
         warp_exclusive_scan(pre, (int)n);
         if constexpr (AGENT_FAST_EDGES > 0 && !App::kWindow) {
