@@ -4,7 +4,7 @@ C ABI.  BFS is checked bit-exact against the serial oracle; PageRank variants ag
 deterministic multithreaded pull-Jacobi (time-boxed).  The oracle is test infrastructure.
 Prints one JSON line.  Not part of the product path."""
 import argparse, json, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import graphgen as gg
 import paper_2112_00132_b200 as atos

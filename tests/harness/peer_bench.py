@@ -4,13 +4,13 @@ run as one persistent kernel.  All partitions share the SMs and HBM, so this
 measures the protocol's overhead (remote pushes, summed termination), not
 multi-GPU scaling.  Not the product path; parity is in tests/test_peer.py.
 
-usage: python tools/peer_bench.py [--scale 22] [--runs 3]
+usage: python tests/harness/peer_bench.py [--scale 22] [--runs 3]
 """
 import argparse
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import graphgen as gg  # noqa: E402

@@ -3,7 +3,7 @@ timing it: BFS exact, PageRank within 1e-4, colouring valid.  Not a test."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import graphgen as gg  # noqa: E402

@@ -11,7 +11,7 @@ C2: RMAT-16 (ef 16, seed 1): PageRank alpha=.85 eps=1e-6 (ms, GTEPS_raw, GTEPS_n
     tasks / 2n, validity).
 """
 import os, sys, statistics
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import graphgen as gg
 import oracle
