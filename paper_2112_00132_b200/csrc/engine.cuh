@@ -32,6 +32,9 @@ struct GraphView {
 
 // ------------------------------------------------------------------ apps ---
 
+#ifndef ATOS_BFS_NODONE
+#define ATOS_BFS_NODONE 0  // experiment: no expanded-at-depth dedupe (R25)
+#endif
 // Speculative BFS relax (Alg. 2): d = current dist[v] (R3);
 // per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
 // (strict, R2).
@@ -111,7 +114,12 @@ struct BfsApp {
   __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
     p = x.d + 1u;
     if (x.e1 == x.e0) return false;
+#if ATOS_BFS_NODONE
+    (void)v;
+    return true;
+#else
     return atomicMin(done + v, x.d) > x.d;
+#endif
   }
   __device__ __forceinline__ bool edge(Payload nd, uint32_t w, uint32_t tag) const {
     const Probe pr = probe(w, tag);

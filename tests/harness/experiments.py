@@ -6,7 +6,8 @@
   color     greedy colouring on RMAT-16 (configs[1]): time-to-colour, colours vs the
             oracle, overwork; permuted vs unpermuted ids; all kernels/workers
   grid      BFS on the 24M-vertex grid and the road-like variant: ms, per-hop latency
-  timeline  cumulative work vs time for BFS/PR on RMAT-24
+  timeline  cumulative work vs time for BFS/PR on RMAT-24, colouring on RMAT-22
+  colorq    colour count vs concurrency (workers in flight), RMAT-20, plain and permuted ids
 """
 import os
 import statistics
@@ -141,6 +142,31 @@ def grid():
             e = int(d[reached].max())
             print(f"| {gname} | {label} ({t}) | {f} | {ms:.1f} | {ms * 1e3 / e:.2f} (ecc {e}, reached "
                   f"{int(reached.sum())}) | {st['tasks_popped'] / reached.sum():.3f} |", flush=True)
+
+
+def colorq():
+    """Colour count vs concurrency (855 colours vs the oracle's 464 on RMAT-24):
+    speculative colouring picks the smallest colour free among the neighbours' colours as they are
+    at that moment; with thousands of tasks in flight a vertex often sees neighbours still uncoloured
+    or about to change, and conflicts re-colour the larger id with a larger colour.  Fewer concurrent
+    workers should approach the serial id-order greedy count."""
+    import oracle
+    for perm in (0, 7):
+        s = gg.rmat(20, 16, seed=1, symmetrize=True, perm_seed=perm)
+        S = atos.Graph.from_csr(s, symmetric=True)
+        _, k_or = oracle.greedy_color(s)
+        print(f"\n### Colours vs concurrency, RMAT-20 symmetrised{' (permuted ids)' if perm else ''}: "
+              f"oracle id-order greedy = {k_or}\n")
+        print("| worker | CTAs (num_blocks) | threads | F | tasks in flight (max) | ms | colours | colours / oracle | tasks / 2n |")
+        print("|---|---|---|---|---|---|---|---|---|")
+        for w, blocks, t, f in [("thread", 1, 32, 1), ("warp", 1, 32, 1), ("cta", 1, 128, 32), ("cta", 8, 128, 32),
+                                ("cta", 32, 128, 32), ("cta", 148, 256, 32), ("cta", 0, 256, 32),
+                                ("cta", 0, 256, 128)]:
+            (c, k, st), ms = timed3(lambda: atos.color(S, worker=w, num_blocks=blocks, cta_threads=t, fetch_size=f,
+                                                      timeout_s=300), 2)
+            flight = "all resident" if blocks == 0 else str(blocks * (f if w == "cta" else (t // 32) * f * (32 if w == "thread" else 1)))
+            print(f"| {w} | {blocks or 'max'} | {t} | {f} | {flight} | {ms:.1f} | {k} | {k / k_or:.2f} | "
+                  f"{st['tasks_popped'] / (2 * s.n):.2f} |", flush=True)
 
 
 def timeline():

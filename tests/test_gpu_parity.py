@@ -140,6 +140,21 @@ def test_bfs_serial_order_identity(atos):
             assert st["tasks_popped"] == want, (name, defer)
 
 
+@pytest.mark.parametrize("name", ["rmat12s", "grid64", "K9", "two"])
+def test_color_serial_order_identity(atos, name):
+    """One warp worker, FETCH 1, one CTA: the queue is strictly FIFO, so every
+    ASSIGN(v) (queued in id order, R22) runs after every ASSIGN(u < v) and
+    before any CHECK — exactly the oracle's serial id-order greedy:
+    the same colour for every vertex, not just the same count.  More tasks in
+    flight raise the count (tests/harness/experiments.py colorq)."""
+    g = G(name)
+    exp, k_or = oracle.greedy_color(g)
+    c, k, st = atos.color(D(atos, name, symmetric=True), worker="warp", fetch_size=1, num_blocks=1, cta_threads=32)
+    assert np.array_equal(c, exp)
+    assert k == k_or
+    assert st["tasks_popped"] == 2 * g.n  # one ASSIGN and one CHECK each, no conflict
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("worker", WORKERS)
 def test_bfs_sink_defer(atos, kernel, worker):
