@@ -894,7 +894,6 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
   const bool bsp = c.cfg.kernel == ATOS_KERNEL_BSP;
   CKS(ws_prepare(g, c.cfg, n, 2 * (uint64_t)n, !bsp, c.s));
   CKS(ensure(w.u32a, w.u32a_n, (size_t)n));
-  CKS(ensure(w.u32b, w.u32b_n, (size_t)n));
   CKS(ensure(w.u16a, w.u16a_n, (size_t)n));
   if (bsp) {
     CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
@@ -903,12 +902,12 @@ extern "C" atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cf
   CK(cudaEventRecord(w.ev[0], c.s));
   CKS(ring_reset(w, c.s));
   // a2: init (timed)
-  k_bfs_init<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, w.u32b, w.u16a, n, src);
+  k_bfs_init<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.u32a, nullptr, w.u16a, n, src);
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : 1, w.ring, bsp ? -1 : src);
   CK(cudaGetLastError());
   c.launches += 2;
   CK(cudaEventRecord(w.ev[1], c.s));
-  BfsApp app{w.u32a, w.u32b, w.u16a, c.cfg.bfs_filter, c.cfg.sink_defer ? g->d_sink : nullptr,
+  BfsApp app{w.u32a, w.u16a, c.cfg.bfs_filter, c.cfg.sink_defer ? g->d_sink : nullptr,
              g->d_hub != nullptr ? 1u : 0u};
   c.split = c.cfg.hub_split != 0;  // R24: on by default for BFS
   using P = EdgeMapPolicy<BfsApp>;

@@ -32,9 +32,6 @@ struct GraphView {
 
 // ------------------------------------------------------------------ apps ---
 
-#ifndef ATOS_BFS_NODONE
-#define ATOS_BFS_NODONE 0  // experiment: no expanded-at-depth dedupe (R25)
-#endif
 // Speculative BFS relax (Alg. 2): d = current dist[v] (R3);
 // per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
 // (strict, R2).
@@ -42,7 +39,6 @@ struct BfsApp {
   static constexpr bool kWindow = false;
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   uint32_t* dist;
-  uint32_t* done;  // done[v] = smallest depth at which v has been expanded (init MAX)
   // near[v] = min(dist[v], 0xFFFF) as of some moment (stale values are larger,
   // never smaller): a 2-byte mirror of dist that the per-edge filter probes.
   // At 32 MB (RMAT-24) it stays L2-resident where the 64 MB dist array
@@ -88,9 +84,6 @@ struct BfsApp {
     if (sink == nullptr) return true;
     return sink_tagged ? !(pr >> 31) : !((ld_nc_u32(sink + (w >> 5)) >> (w & 31)) & 1u);
   }
-  // Expand v at its CURRENT depth d (R3) unless some task already expanded
-  // (or is expanding) v at depth <= d: a vertex pushed k times by k
-  // improvements is expanded at most once per distinct depth it is popped at.
   __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1,
                                         Payload& p) const {
     Pre x = begin_load(v, g);
@@ -111,15 +104,14 @@ struct BfsApp {
     x.d = ld_relaxed_hot(dist + v);
     return x;
   }
-  __device__ __forceinline__ bool begin_commit(uint32_t v, const Pre& x, Payload& p) const {
+  // Expand v at its CURRENT depth d (R3).  No "expanded once per depth"
+  // dedupe (R25): its atomicMin on a per-vertex word sat on the queue agent's
+  // critical path (one more dependent L2 round trip per batch) and cost more
+  // than the duplicate expansions it saved (RMAT-24: 3.5 -> 2.75 ms for +2.5%
+  // edge visits, profiles/r02_bfs_variants.md).
+  __device__ __forceinline__ bool begin_commit(uint32_t, const Pre& x, Payload& p) const {
     p = x.d + 1u;
-    if (x.e1 == x.e0) return false;
-#if ATOS_BFS_NODONE
-    (void)v;
-    return true;
-#else
-    return atomicMin(done + v, x.d) > x.d;
-#endif
+    return x.e1 != x.e0;
   }
   __device__ __forceinline__ bool edge(Payload nd, uint32_t w, uint32_t tag) const {
     const Probe pr = probe(w, tag);

@@ -365,7 +365,7 @@ __global__ void k_ctl_init(QueueCtl* ctl, uint64_t tail, uint64_t* ring, int64_t
 __global__ void k_bfs_init(uint32_t* dist, uint32_t* done, uint16_t* near, int64_t n, int64_t src) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     dist[i] = (i == src) ? 0u : 0xFFFFFFFFu;
-    done[i] = 0xFFFFFFFFu;
+    if (done) done[i] = 0xFFFFFFFFu;
     if (near) near[i] = (i == src) ? (uint16_t)0 : (uint16_t)0xFFFFu;
   }
 }
