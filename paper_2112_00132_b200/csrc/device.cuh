@@ -594,12 +594,15 @@ __device__ __forceinline__ void q_thread_push(const Queue& q, uint32_t k, F item
 // head never passes tail (no overshoot).  Producers publish after reserving
 // tail and storing, so a claimed slot is at worst an in-flight store.
 // Returns the count claimed (0 if nothing is published right now).
+#ifndef ATOS_POP_HINT_MIN
+#define ATOS_POP_HINT_MIN 8ll  // skip the pre-read when the caller last saw > this many batches queued
+#endif
 __device__ __forceinline__ uint32_t q_try_pop(const Queue& q, uint32_t want, uint64_t& first, uint64_t& qlen,
                                               long long hint = 0) {
   long long* cnt = reinterpret_cast<long long*>(&q.ctl->count.v);
   // Skip the pre-read when the caller's last observation says the queue is
   // long (saves one L2 round trip per pop on the critical path).
-  const long long seen = hint > 8ll * (long long)want ? hint : (long long)ld_relaxed_u64(&q.ctl->count.v);
+  const long long seen = hint > ATOS_POP_HINT_MIN * (long long)want ? hint : (long long)ld_relaxed_u64(&q.ctl->count.v);
   if (seen <= 0) return 0;
   // Adaptive fetch: while the queue is short, take only a fair share
   // ceil(count / workers) (>= 1) so a small frontier — e.g. the ~200 chunk
