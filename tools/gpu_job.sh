@@ -1,7 +1,15 @@
 # ad-hoc GPU job (overwritten per experiment; the committed copy is the last one run)
 python -c "import __graft_entry__ as e; e.build()" > gpurun_out/build.log 2>&1
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench_rc=$?; tail -c 300 gpurun_out/bench.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1_rc=$?
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_persistent -c 1 -o gpurun_out/bfs_full3 -f python tools/profile_run.py --app bfs --threads 256 --fetch 128 --iters 1 > gpurun_out/ncu_bfs.log 2>&1; echo ncu3_rc=$?
-timeout 600 ncu --section PmSampling --section PmSampling_WarpStates --section LaunchStats --section Occupancy --clock-control none -k regex:k_persistent -c 1 -o gpurun_out/bfs_pm3 -f python tools/profile_run.py --app bfs --threads 256 --fetch 128 --iters 1 > gpurun_out/ncu_pm_bfs.log 2>&1; echo pm=$?
-timeout 600 python tests/harness/experiments.py timeline > gpurun_out/timeline.md 2>&1; echo tl=$?
+VD=paper_2112_00132_b200/variants
+for v in a2n8 a2n6; do ATOS_LIB=$VD/libatos_$v.so timeout 120 python tests/harness/quick_check.py >> gpurun_out/qc.log 2>&1; echo "$v rc=$?" >> gpurun_out/qc.log; done; tail -4 gpurun_out/qc.log
+for rep in 1 2; do
+for lib in product a2n8 a2n6; do
+  if [ $lib = product ]; then L=""; V='{"f128": {"cta_threads": 1024}, "f64": {"cta_threads": 1024, "fetch_size": 64}}'; fi
+  if [ $lib = a2n8 ]; then L=$VD/libatos_$lib.so; V='{"f64": {"cta_threads": 1024, "fetch_size": 64}, "f32": {"cta_threads": 1024, "fetch_size": 32}}'; fi
+  if [ $lib = a2n6 ]; then L=$VD/libatos_$lib.so; V='{"f96": {"cta_threads": 1024, "fetch_size": 96}, "f64": {"cta_threads": 1024, "fetch_size": 64}}'; fi
+  grep -q "$lib rc=0" gpurun_out/qc.log || [ $lib = product ] || continue
+  echo "== $lib rep $rep" >> gpurun_out/nbf.md
+  ATOS_LIB=$L timeout 300 python tests/harness/pr_variants.py --runs 2 --no-oracle --variants "$V" >> gpurun_out/nbf.md 2>&1
+done; done
+ATOS_LIB=$VD/libatos_wprof.so timeout 300 python tests/harness/pr_variants.py --runs 1 --no-oracle --variants '{"t1024": {"cta_threads": 1024}}' > gpurun_out/wprof2.md 2>&1
+ATOS_LIB=$VD/libatos_wprof.so timeout 300 python tests/harness/pr_variants.py --app bfs --runs 1 --no-oracle --variants '{"t256": {"cta_threads": 256}}' >> gpurun_out/wprof2.md 2>&1
