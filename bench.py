@@ -135,20 +135,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def atomic_ceiling(e_pr, kms):
+def atomic_ceiling(e_pr, kms, args):
+    """Edge pushes per second against the L2 atomic ceiling for THIS graph's target distribution:
+    tools/atomic_trace.py replays RMAT-24's column array through the R35 push (red.add.f64 at hubs,
+    returning f32 atomicAdd elsewhere), profiles/r02_atomic_ceiling.json.  The random-address
+    ceilings of tools/ubench.cu are reported beside it."""
     ach = statistics.mean(e / (k * 1e-3) / 1e9 for e, k in zip(e_pr, kms))
+    out = {"achieved_gops": ach, "atom_uniform_gops": ATOM_UNIFORM_GOPS, "atom_skewed_gops": ATOM_SKEWED_GOPS,
+           "red_f64_skewed_gops": RED_SKEWED_GOPS}
     try:
-        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
-            t = json.load(f)["pagerank_persistent_cta"]
-        red = t["red_sectors"] / (t["red_sectors"] + t["atom_sectors"])
+        with open(os.path.join(ROOT, "profiles", "r02_atomic_ceiling.json")) as f:
+            c = json.load(f)[f"rmat{args.scale}_ef{args.edge_factor}_s1"]
+        out.update(peak_gops=c["mixed_r35_gops"], frac=ach / c["mixed_r35_gops"], source=c["source"])
     except Exception:
-        red = 0.0
-    peak = 1.0 / ((1 - red) / ATOM_SKEWED_GOPS + red / RED_SKEWED_GOPS)
-    return {"achieved_gops": ach, "peak_gops": peak, "frac": ach / peak, "red_share": red,
-            "atom_skewed_gops": ATOM_SKEWED_GOPS, "red_f64_skewed_gops": RED_SKEWED_GOPS,
-            "atom_uniform_gops": ATOM_UNIFORM_GOPS,
-            "source": "profiles/r02_ubench_sweep.md (skewed returning f32 atomicAdd / red.add.f64), red share "
-                      "from profiles/r02_traffic.json (ncu lts__t_sectors_srcunit_tex_op_{atom,red})"}
+        out.update(peak_gops=ATOM_SKEWED_GOPS, frac=ach / ATOM_SKEWED_GOPS,
+                   source="profiles/r02_ubench_sweep.md (no graph-trace ceiling for this workload)")
+    return out
 
 
 def ncu_traffic(key):
@@ -396,11 +398,9 @@ def run_atos(args, rank, world, local_rank):
                                       "frac": pr_sec / (pr_kms * 1e-3) / 1e9 / hbm,
                                       "bytes_model": "36 B/edge push (col 4 + residue sector 32) + 104 B/pop "
                                                      "(off sector 32 + slot 8 + exch sector 32 + rank sector 32)"}},
-        # PageRank's edge push is one L2 atomic on a random, RMAT-skewed address: a returning fp32
-        # atomicAdd (threshold crossing) or, for hub targets (R35), a fire-and-forget red.add.f64; the
-        # ceiling it runs against is the mix of the two measured rates (tools/ubench.cu), weighted by
-        # the red share of the kernel's L2 atomic sectors in the committed ncu capture
-        "atomic_ceiling": atomic_ceiling(e_pr, [r[3]["kernel_ms"] for r in records]),
+        # PageRank's edge push is one L2 atomic on an RMAT-skewed address: a returning fp32 atomicAdd
+        # (threshold crossing) or, for hub targets (R35), a fire-and-forget red.add.f64
+        "atomic_ceiling": atomic_ceiling(e_pr, [r[3]["kernel_ms"] for r in records], args),
         "bfs": {"gteps": e_bfs / (statistics.mean(t_bfs) * 1e-3) / 1e9, "ms": statistics.mean(t_bfs),
                 "kernel_ms": bfs_kms, "edges": e_bfs, "reached": v_bfs,
                 "roofline_frac": bfs_ach / hbm, "achieved_gbs": bfs_ach,
