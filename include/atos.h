@@ -158,9 +158,12 @@ atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t
  * fixed point x = (1-alpha) 1 + alpha P x (R4, R5, R8).  On return every
  * residue is <= eps and 0 <= x^* - rank <= eps x^* / (1-alpha), up to the
  * residues' rounding: fp32 residues, except fp64 at hub vertices (in-degree
- * >= 512, tagged at graph create, R34) — rounding stays below ~3e-5 of each
- * rank — or fp64 everywhere with cfg->pr_residue_fp64, on a graph created
- * with ATOS_GRAPH_BORROW, and on partitioned graphs.  Ranks accumulate in
+ * >= 512, tagged at graph create, R34) — rounding stays below 512 2^-24 of
+ * each rank (R36) — or fp64 everywhere with cfg->pr_residue_fp64, on a graph
+ * created with ATOS_GRAPH_BORROW, and on partitioned / peer graphs.  With
+ * persistent CTA workers hub targets take fire-and-forget fp64 adds and are
+ * activated by sweeps (cfg->pr_hub_check, R35); the run ends only after a
+ * clean sweep of every hub, so the residue bound holds at every vertex.  Ranks accumulate in
  * fp64 and are returned as float.  rank_out: float[n].  Errors:
  * INVALID_ARGUMENT (alpha not in (0,1), eps <= 0 or NaN), QUEUE_OVERFLOW,
  * TIMEOUT, CUDA; UNSUPPORTED for Check_Size window activation outside
