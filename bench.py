@@ -514,7 +514,7 @@ def run_atos_multi(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     deg = g.degrees()
-    vb, ve = int(pg.bounds[rank]), int(pg.bounds[rank + 1])
+    vb, ve = pg.v_begin, pg.v_end
 
     def step():
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]

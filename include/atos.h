@@ -277,7 +277,7 @@ atos_status atos_graph_create_peer(int32_t parts, const int32_t* devices, const 
                                    atos_graph* out);
 
 /* Graph-lifetime device memory comes from a private stream-ordered pool that
- * keeps up to 8 GB of freed memory mapped for reuse by the next graph
+ * keeps up to 32 GB of freed memory mapped for reuse by the next graph
  * (DESIGN §5).  atos_pool_trim releases all but keep_bytes of it to the
  * device; atos_pool_reserved reports what the pool currently holds. */
 atos_status atos_pool_trim(uint64_t keep_bytes);
