@@ -957,7 +957,7 @@ static atos_status pagerank_run(LaunchCtx& c, Residues<R> rs, double* rank, floa
   if constexpr (std::is_same<R, float>::value) {
     // tagged graph: fp32 sums for non-hubs, fp64 at hubs (PrInitSplitApp)
     k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rs.res, n, 0.f);
-    k_zero_hubs<<<fill_blocks((n + 31) / 32, g->sms), 256, 0, c.s>>>(rs.hub, n, rs.res64);
+    k_zero_hubs<<<fill_blocks((n + 31) / 32, g->sms), 256, 0, c.s>>>(rs.hub, n, rs.res64, rs.r2);
     PrInitSplitApp ia{rs.res, rs.res64, (1.0 - (double)alpha) * (double)alpha};
     CKS((bsp_step_w<EdgeMapPolicy<PrInitSplitApp>, PrInitSplitApp, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr,
                                                                          nullptr, 256, nullptr)));
@@ -1081,15 +1081,16 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   CKS(ensure(w.f32a, w.f32a_n, (size_t)n));
   CKS(ensure(w.f64a, w.f64a_n, (size_t)n));
   CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // queued flags (window activation f1; hubs R35)
-  CKS(ensure(w.f64b, w.f64b_n, (size_t)n));  // fp64 residues (all, or the hubs') = the seeding sums (R30)
+  // fp64 residues: all of them (untagged / pr_residue_fp64), or the hubs' in two replicas (R34, R38)
+  CKS(ensure(w.f64b, w.f64b_n, (size_t)n * (r64 ? 1 : 2)));
   if (!r64) CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
   if (bsp) {
     CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
     CKS(ensure(w.front[1], w.front_n[1], (size_t)n));
   }
   double* rank = w.f64a;
-  const Residues<double> rs64{w.f64b, nullptr, nullptr};
-  const Residues<float> rs32{w.f32b, w.f64b, g->d_hub};
+  const Residues<double> rs64{w.f64b, nullptr, nullptr, 0};
+  const Residues<float> rs32{w.f32b, w.f64b, g->d_hub, n};  // hub residues: two replicas n apart (R38)
   if (r64) CKS(pagerank_run<double>(c, rs64, rank, alpha, eps));
   else CKS(pagerank_run<float>(c, rs32, rank, alpha, eps));
   c.post_launches = st ? 2 : 1;

@@ -89,7 +89,7 @@ __device__ __forceinline__ uint32_t hub_sweep(const App& app, const Queue& q) {
     for (int k = 0; k < AGENT_G; ++k) {
       const uint32_t j = i + lane_id() + 32 * k;
       v[k] = j < app.hub_check ? __ldg(app.hubs + (uint32_t)((s + j) % app.num_hubs)) : 0xFFFFFFFFu;
-      r[k] = v[k] != 0xFFFFFFFFu ? __ldcg(app.rs.res64 + v[k]) : 0.0;
+      r[k] = v[k] != 0xFFFFFFFFu ? app.rs.hub_read(v[k]) : 0.0;
     }
     bool act[AGENT_G];
 #pragma unroll
@@ -125,7 +125,7 @@ __device__ __forceinline__ int hub_final_sweep(const App& app, const Queue& q, u
     for (int k = 0; k < AGENT_G; ++k) {
       const uint32_t j = b + lane_id() + 32 * k;
       v[k] = j < app.num_hubs ? __ldg(app.hubs + j) : 0xFFFFFFFFu;
-      r[k] = v[k] != 0xFFFFFFFFu ? __ldcg(app.rs.res64 + v[k]) : 0.0;
+      r[k] = v[k] != 0xFFFFFFFFu ? app.rs.hub_read(v[k]) : 0.0;
     }
     bool act[AGENT_G];
 #pragma unroll

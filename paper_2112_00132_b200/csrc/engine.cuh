@@ -154,6 +154,13 @@ struct Residues {
   R* res;                // fp32 (or fp64 with R = double) residue per vertex
   double* res64;         // hub residues (R == float on a tagged graph), indexed by vertex id; else nullptr
   const uint32_t* hub;   // bit v = v is a hub (pops); nullptr when res64 is
+  // R38: a hub's fp64 residue is the sum of two replicas, res64[v] and
+  // res64[r2 + v] (r2 = n): R35's fire-and-forget hub pushes alternate between
+  // them by lane, halving the contention on a hub's L2 line (RMAT-24 target
+  // replay: 92.7 -> 115.6 G ops/s, profiles/r02_atomic_trace.md).  Every reader
+  // sums both; paths that test a crossing write replica 0 only.
+  int64_t r2;
+  __device__ __forceinline__ double hub_read(uint32_t v) const { return __ldcg(res64 + v) + __ldcg(res64 + r2 + v); }
   __device__ __forceinline__ bool is_hub(uint32_t v) const { return res64 && test_bit(hub, v); }
   // Alg. 4 line 7, r = atomicExch(residue[v], 0), in two phases so the hub
   // test never delays the common case: take_issue starts the fp32 exchange
@@ -170,7 +177,8 @@ struct Residues {
     return t;
   }
   __device__ __forceinline__ double take_finish(uint32_t v, const Take& t) const {
-    return ((t.word >> (v & 31)) & 1u) ? atomic_take(res64 + v) + (double)t.r : (double)t.r;
+    return ((t.word >> (v & 31)) & 1u) ? atomic_take(res64 + v) + atomic_take(res64 + r2 + v) + (double)t.r
+                                       : (double)t.r;
   }
   __device__ __forceinline__ double take(uint32_t v) const { return take_finish(v, take_issue(v)); }
   // residue[w] += c at the storage the column's hub tag names; returns the old value
@@ -188,7 +196,7 @@ struct Residues {
     return (R)old <= eps && add_rn((R)old, c) > eps;
   }
   __device__ __forceinline__ double peek(uint32_t v) const {  // L2 read (sweeps)
-    return is_hub(v) ? __ldcg(res64 + v) : (double)__ldcg(res + v);
+    return is_hub(v) ? hub_read(v) : (double)__ldcg(res + v);
   }
   // put a taken residue back (deferral); returns the old value
   __device__ __forceinline__ double put(uint32_t v, double r) const {
@@ -200,6 +208,9 @@ struct Residues {
 // r = atomicExch(res[v], 0); rank[v] += r; c = alpha r / deg(v);
 // per edge: old = atomicAdd(res[w], c); push w iff old <= eps < old + c.
 // rank accumulates in fp64 (a per-pop cost): a hub receives 10^4+ pops.
+#ifndef ATOS_HUB_REPLICAS
+#define ATOS_HUB_REPLICAS 2u  // R38: 1 or 2
+#endif
 #ifndef ATOS_PR_AGENTS
 #define ATOS_PR_AGENTS 2
 #endif
@@ -288,7 +299,7 @@ struct PrAppT {
   __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
     if constexpr (HS) {
       if (tag & TAG_HUB) {  // R35: hub target, activated by sweeps
-        red_add_hot(rs.res64 + w, (double)c);
+        red_add_hot(rs.res64 + (lane_id() & (ATOS_HUB_REPLICAS - 1u)) * rs.r2 + w, (double)c);  // R38 replica by lane
         return 0.0;
       }
     }

@@ -10,6 +10,9 @@
 //   mixed  red.add.f64 for targets whose column carries HUB_TAG (bit 31; in-degree
 //          >= 512, R34/R35) and returning f32 atomicAdd for the others — the
 //          product's R35 push
+//   mixed, R replicas  the same with each hub's fp64 residue spread over R
+//          arrays n elements apart (replica = lane bits): what splitting a hub's
+//          residue would buy against hot-line contention
 // Input: a raw int32 file of column entries (tools/atomic_trace.py writes it).
 // Prints G ops/s per mode.  Not part of the product.
 #include <cstdint>
@@ -20,7 +23,7 @@
 #include <cuda_runtime.h>
 
 template <int MODE>
-__global__ void k(const uint32_t* __restrict__ col, int64_t m, float* res, double* res64, float* sink) {
+__global__ void k(const uint32_t* __restrict__ col, int64_t m, float* res, double* res64, float* sink, int64_t nrep) {
   constexpr int U = 8;
   float acc = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
@@ -38,6 +41,12 @@ __global__ void k(const uint32_t* __restrict__ col, int64_t m, float* res, doubl
       if (MODE == 1) asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(res + v), "f"(1e-7f));
       if (MODE == 2) {
         if (w[j] & 0x80000000u) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(res64 + v), "d"(1e-7));
+        else r[j] = atomicAdd(res + v, 1e-7f);
+      }
+      if (MODE >= 3) {  // hub residues spread over R = 2^(MODE-2) replica arrays (replica = lane bits)
+        constexpr int R = 1 << (MODE >= 3 ? MODE - 2 : 0);
+        const int64_t rep = (int64_t)(threadIdx.x & (R - 1)) * (int64_t)nrep;
+        if (w[j] & 0x80000000u) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(res64 + rep + v), "d"(1e-7));
         else r[j] = atomicAdd(res + v, 1e-7f);
       }
     }
@@ -66,26 +75,31 @@ int main(int argc, char** argv) {
   double* res64;
   cudaMalloc(&col, m * 4);
   cudaMalloc(&res, n * 4);
-  cudaMalloc(&res64, n * 8);
+  cudaMalloc(&res64, n * 8 * 8);  // up to 8 replica arrays (modes 3-5)
   cudaMalloc(&s, 4);
   cudaMemcpy(col, h.data(), m * 4, cudaMemcpyHostToDevice);
   cudaMemset(res, 0, n * 4);
-  cudaMemset(res64, 0, n * 8);
+  cudaMemset(res64, 0, n * 8 * 8);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const char* names[] = {"atom.add.f32 (returning) on every target", "red.add.f32 on every target",
-                         "mixed: red.add.f64 at hub targets, returning atom.add.f32 elsewhere (R35)"};
+                         "mixed: red.add.f64 at hub targets, returning atom.add.f32 elsewhere (R35)",
+                         "mixed, hub residues over 2 replica arrays", "mixed, hub residues over 4 replica arrays",
+                         "mixed, hub residues over 8 replica arrays"};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   printf("| op | targets (edges) | ms | G ops/s |\n|---|---|---|---|\n");
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 6; ++mode) {
     float ms = 0;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(e0);
-      if (mode == 0) k<0><<<sms * 8, 256>>>(col, m, res, res64, s);
-      if (mode == 1) k<1><<<sms * 8, 256>>>(col, m, res, res64, s);
-      if (mode == 2) k<2><<<sms * 8, 256>>>(col, m, res, res64, s);
+      if (mode == 0) k<0><<<sms * 8, 256>>>(col, m, res, res64, s, n);
+      if (mode == 1) k<1><<<sms * 8, 256>>>(col, m, res, res64, s, n);
+      if (mode == 2) k<2><<<sms * 8, 256>>>(col, m, res, res64, s, n);
+      if (mode == 3) k<3><<<sms * 8, 256>>>(col, m, res, res64, s, n);
+      if (mode == 4) k<4><<<sms * 8, 256>>>(col, m, res, res64, s, n);
+      if (mode == 5) k<5><<<sms * 8, 256>>>(col, m, res, res64, s, n);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1);
