@@ -93,7 +93,7 @@ typedef struct {
                           /*   2048-edge chunk tasks (R24).  -1 = app default (BFS on, PageRank  */
                           /*   off: R33), 0 = off, 1 = on                                         */
   int32_t pr_hub_check;   /* PageRank, persistent CTA workers with fp32 residues: hub targets    */
-                          /*   (in-degree >= 512) take fire-and-forget fp64 adds and are       */
+                          /*   (in-degree >= 2048) take fire-and-forget fp64 adds and are      */
                           /*   activated by sweeps — this many hubs checked per processed batch */
                           /*   (R35; default 16); 0 = threshold crossing at hubs too (R34)      */
 } atos_config;
@@ -136,7 +136,7 @@ void atos_config_default(atos_config* cfg);
 /* Build a graph handle from CSR: row_offsets int64[n+1], col_indices int32[m]
  * (P:427 vertex.neighbors; S:26-37 invariants).  Copies to the device unless
  * ATOS_GRAPH_BORROW|ATOS_GRAPH_DEVICE_PTRS.  A copied CSR gets hub tags (bit
- * 31 of a column entry = its target's in-degree is >= 512, R34; internal to
+ * 31 of a column entry = its target's in-degree is >= 2048, R34; internal to
  * the library).  m may exceed 2^31.  n == 0 is allowed.  Errors: INVALID_ARGUMENT (n<0, m<0, NULL pointers with m>0, out==NULL),
  * UNSUPPORTED (n >= 2^30-1), INVALID_GRAPH (with VALIDATE), OUT_OF_MEMORY, CUDA. */
 atos_status atos_graph_create(const int64_t* row_offsets, const int32_t* col_indices, int64_t n,
@@ -158,7 +158,7 @@ atos_status atos_bfs(atos_graph g, int64_t src, const atos_config* cfg, uint32_t
  * fixed point x = (1-alpha) 1 + alpha P x (R4, R5, R8).  On return every
  * residue is <= eps and 0 <= x^* - rank <= eps x^* / (1-alpha), up to the
  * residues' rounding: fp32 residues, except fp64 at hub vertices (in-degree
- * >= 512, tagged at graph create, R34) — rounding stays below 512 2^-24 of
+ * >= 2048, tagged at graph create, R34) — rounding stays below 2048 2^-25 of
  * each rank (R36) — or fp64 everywhere with cfg->pr_residue_fp64, on a graph
  * created with ATOS_GRAPH_BORROW, and on partitioned / peer graphs.  With
  * persistent CTA workers hub targets take fire-and-forget fp64 adds and are

@@ -137,7 +137,7 @@ constexpr int TAG_SHIFT = 30;
 constexpr uint32_t TAG_HUB = HUB_TAG >> TAG_SHIFT;    // 2
 constexpr uint32_t TAG_SINK = SINK_TAG >> TAG_SHIFT;  // 1
 #ifndef ATOS_HUB_IN_DEG
-#define ATOS_HUB_IN_DEG 512
+#define ATOS_HUB_IN_DEG 2048  // R34 (512 until the R38 replicas; 2048: -8% PageRank, profiles/r02_hub_threshold.md)
 #endif
 constexpr uint32_t HUB_IN_DEG = ATOS_HUB_IN_DEG;
 // streaming read-only loads of immutable CSR arrays (no L1 allocation, L2 evict-first)

@@ -123,14 +123,14 @@ struct BfsApp {
 // except at HUB vertices — in-degree >= HUB_IN_DEG, tagged in the CSR at
 // graph create (device.cuh HUB_TAG) — whose residues are fp64 in res64.  A
 // residue that keeps growing while its vertex waits in the queue rounds away
-// the small pushes it receives: k adds onto an fp32 sum lose up to k 2^-24 of
-// the accumulated mass, and identical pushes (a fan-in hub fed by equal-degree
-// chains) round the same way every time — measured 2.3e-4 of max x* on a
-// 40,000-way fan-in (above the 1e-4 gate).  A vertex receives at most about
-// in-degree adds per queue cycle, so below HUB_IN_DEG = 512 the loss is
-// < 512 2^-24 = 3.1e-5 of its rank even if every rounding had the same sign;
-// at hubs fp64 makes it negligible.  RMAT-24: 55 K hubs take 46% of the edge
-// pushes, on L2-resident lines.  (A TwoSum-compensated fp32 add, tried first,
+// the small pushes it receives: each of k adds onto an fp32 sum rounds by at
+// most half an ulp, 2^-25 of the sum, and identical pushes (a fan-in hub fed
+// by equal-degree chains) round the same way every time — measured 2.3e-4 of
+// max x* on a 40,000-way fan-in (above the 1e-4 gate).  A vertex receives at
+// most about in-degree adds per queue cycle, so below HUB_IN_DEG = 2048 the
+// loss is < 2048 2^-25 = 6.1e-5 of its rank even if every rounding had the
+// same sign; at hubs fp64 makes it negligible.  RMAT-24: 12,951 hubs take
+// 27% of the edge pushes.  (A TwoSum-compensated fp32 add, tried first,
 // cost +40% on RMAT-24; fp64 residues everywhere +10%.)  With R = double
 // (atos_config.pr_residue_fp64, untagged graphs) every residue is fp64.
 __device__ __forceinline__ float atomic_take(float* p) { return atomicExch(p, 0.0f); }
