@@ -1082,7 +1082,7 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   CKS(ensure(w.f64a, w.f64a_n, (size_t)n));
   CKS(ensure(w.u32a, w.u32a_n, (size_t)n));  // queued flags (window activation f1; hubs R35)
   // fp64 residues: all of them (untagged / pr_residue_fp64), or the hubs' in two replicas (R34, R38)
-  CKS(ensure(w.f64b, w.f64b_n, (size_t)n * (r64 ? 1 : 2)));
+  CKS(ensure(w.f64b, w.f64b_n, (size_t)n * (r64 ? 1 : ATOS_HUB_REPLICAS)));
   if (!r64) CKS(ensure(w.f32b, w.f32b_n, (size_t)n));
   if (bsp) {
     CKS(ensure(w.front[0], w.front_n[0], (size_t)n));
@@ -1090,7 +1090,7 @@ extern "C" atos_status atos_pagerank(atos_graph g, float alpha, float eps, const
   }
   double* rank = w.f64a;
   const Residues<double> rs64{w.f64b, nullptr, nullptr, 0};
-  const Residues<float> rs32{w.f32b, w.f64b, g->d_hub, n};  // hub residues: two replicas n apart (R38)
+  const Residues<float> rs32{w.f32b, w.f64b, g->d_hub, n};  // hub residues: ATOS_HUB_REPLICAS replicas n apart (R38)
   if (r64) CKS(pagerank_run<double>(c, rs64, rank, alpha, eps));
   else CKS(pagerank_run<float>(c, rs32, rank, alpha, eps));
   c.post_launches = st ? 2 : 1;

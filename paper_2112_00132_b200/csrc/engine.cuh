@@ -119,6 +119,9 @@ struct BfsApp {
   }
 };
 
+#ifndef ATOS_HUB_REPLICAS
+#define ATOS_HUB_REPLICAS 2u  // R38: hub-residue replicas (a power of two)
+#endif
 // PageRank residue storage (R34).  Residues are fp32 (4 B per edge push)
 // except at HUB vertices — in-degree >= HUB_IN_DEG, tagged in the CSR at
 // graph create (device.cuh HUB_TAG) — whose residues are fp64 in res64.  A
@@ -160,7 +163,18 @@ struct Residues {
   // replay: 92.7 -> 115.6 G ops/s, profiles/r02_atomic_trace.md).  Every reader
   // sums both; paths that test a crossing write replica 0 only.
   int64_t r2;
-  __device__ __forceinline__ double hub_read(uint32_t v) const { return __ldcg(res64 + v) + __ldcg(res64 + r2 + v); }
+  __device__ __forceinline__ double hub_read(uint32_t v) const {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < (int)ATOS_HUB_REPLICAS; ++k) s += __ldcg(res64 + k * r2 + v);
+    return s;
+  }
+  __device__ __forceinline__ double hub_take(uint32_t v) const {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < (int)ATOS_HUB_REPLICAS; ++k) s += atomic_take(res64 + k * r2 + v);
+    return s;
+  }
   __device__ __forceinline__ bool is_hub(uint32_t v) const { return res64 && test_bit(hub, v); }
   // Alg. 4 line 7, r = atomicExch(residue[v], 0), in two phases so the hub
   // test never delays the common case: take_issue starts the fp32 exchange
@@ -177,8 +191,7 @@ struct Residues {
     return t;
   }
   __device__ __forceinline__ double take_finish(uint32_t v, const Take& t) const {
-    return ((t.word >> (v & 31)) & 1u) ? atomic_take(res64 + v) + atomic_take(res64 + r2 + v) + (double)t.r
-                                       : (double)t.r;
+    return ((t.word >> (v & 31)) & 1u) ? hub_take(v) + (double)t.r : (double)t.r;
   }
   __device__ __forceinline__ double take(uint32_t v) const { return take_finish(v, take_issue(v)); }
   // residue[w] += c at the storage the column's hub tag names; returns the old value
@@ -208,9 +221,6 @@ struct Residues {
 // r = atomicExch(res[v], 0); rank[v] += r; c = alpha r / deg(v);
 // per edge: old = atomicAdd(res[w], c); push w iff old <= eps < old + c.
 // rank accumulates in fp64 (a per-pop cost): a hub receives 10^4+ pops.
-#ifndef ATOS_HUB_REPLICAS
-#define ATOS_HUB_REPLICAS 2u  // R38: 1 or 2
-#endif
 #ifndef ATOS_PR_AGENTS
 #define ATOS_PR_AGENTS 2
 #endif

@@ -437,8 +437,7 @@ __global__ void k_zero_hubs(const uint32_t* bits, int64_t n, double* res64, int6
     while (m) {
       const int b = __ffs(m) - 1;
       m &= m - 1;
-      res64[w * 32 + b] = 0.0;
-      res64[r2 + w * 32 + b] = 0.0;  // R38 replica
+      for (int k = 0; k < (int)ATOS_HUB_REPLICAS; ++k) res64[k * r2 + w * 32 + b] = 0.0;  // R38 replicas
     }
   }
 }
@@ -523,10 +522,10 @@ __global__ void k_pr_absorb_sinks(const uint32_t* __restrict__ bits, Residues<R>
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     if ((bits[v >> 5] >> (v & 31)) & 1u) {
       const bool h = rs.res64 && bit_of(rs.hub, v);
-      const double r = h ? rs.res64[v] + rs.res64[rs.r2 + v] : (double)rs.res[v];
+      const double r = h ? rs.hub_read((uint32_t)v) : (double)rs.res[v];
       if (r != 0.0) {
         rank[v] += r;
-        if (h) rs.res64[v] = rs.res64[rs.r2 + v] = 0.0;
+        if (h) for (int k = 0; k < (int)ATOS_HUB_REPLICAS; ++k) rs.res64[k * rs.r2 + v] = 0.0;
         else rs.res[v] = R(0);
       }
     }
@@ -540,7 +539,7 @@ __global__ void k_pr_filter(Residues<R> rs, int64_t n, R eps, uint32_t* out, uns
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; b < n; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = b + lane_id();
     bool a = false;
-    if (v < n) a = (rs.res64 && bit_of(rs.hub, v)) ? rs.res64[v] + rs.res64[rs.r2 + v] > (double)eps : rs.res[v] > eps;
+    if (v < n) a = (rs.res64 && bit_of(rs.hub, v)) ? rs.hub_read((uint32_t)v) > (double)eps : rs.res[v] > eps;
     sink.warp_push(a, (uint32_t)v);
   }
 }
@@ -550,7 +549,7 @@ template <class R>
 __global__ void k_max_res(Residues<R> rs, int64_t n, unsigned int* out_bits) {
   float m = 0.f;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    m = fmaxf(m, (rs.res64 && bit_of(rs.hub, i)) ? (float)(rs.res64[i] + rs.res64[rs.r2 + i]) : (float)rs.res[i]);
+    m = fmaxf(m, (rs.res64 && bit_of(rs.hub, i)) ? (float)rs.hub_read((uint32_t)i) : (float)rs.res[i]);
   for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL_MASK, m, d));
   if (lane_id() == 0) atomicMax(out_bits, __float_as_uint(m));  // m >= 0 so bit order == value order
 }
