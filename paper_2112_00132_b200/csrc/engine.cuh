@@ -120,7 +120,7 @@ struct BfsApp {
 };
 
 #ifndef ATOS_HUB_REPLICAS
-#define ATOS_HUB_REPLICAS 2u  // R38: hub-residue replicas (a power of two)
+#define ATOS_HUB_REPLICAS 4u  // R38: hub-residue replicas (a power of two)
 #endif
 // PageRank residue storage (R34).  Residues are fp32 (4 B per edge push)
 // except at HUB vertices — in-degree >= HUB_IN_DEG, tagged in the CSR at
@@ -157,11 +157,12 @@ struct Residues {
   R* res;                // fp32 (or fp64 with R = double) residue per vertex
   double* res64;         // hub residues (R == float on a tagged graph), indexed by vertex id; else nullptr
   const uint32_t* hub;   // bit v = v is a hub (pops); nullptr when res64 is
-  // R38: a hub's fp64 residue is the sum of two replicas, res64[v] and
-  // res64[r2 + v] (r2 = n): R35's fire-and-forget hub pushes alternate between
-  // them by lane, halving the contention on a hub's L2 line (RMAT-24 target
-  // replay: 92.7 -> 115.6 G ops/s, profiles/r02_atomic_trace.md).  Every reader
-  // sums both; paths that test a crossing write replica 0 only.
+  // R38: a hub's fp64 residue is the sum of ATOS_HUB_REPLICAS = 4 replicas,
+  // res64[k r2 + v] (r2 = n): R35's fire-and-forget hub pushes spread over
+  // them by lane, dividing the contention on a hub's L2 line (RMAT-24 target
+  // replay at the 2048 threshold: 92.7 -> 118.6 G ops/s,
+  // profiles/r02_atomic_trace.md).  Every reader sums them; paths that test a
+  // crossing write replica 0 only.
   int64_t r2;
   __device__ __forceinline__ double hub_read(uint32_t v) const {
     double s = 0.0;
