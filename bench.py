@@ -138,7 +138,7 @@ class ClockSampler:
 def atomic_ceiling(e_pr, kms, args):
     """Edge pushes per second against the L2 atomic ceiling for THIS graph's target distribution:
     tools/atomic_trace.py replays RMAT-24's column array through the product's push (R35/R38:
-    red.add.f64 into one of two replicas at hubs, returning f32 atomicAdd elsewhere),
+    red.add.f64 into one of four replicas at hubs, returning f32 atomicAdd elsewhere),
     profiles/r02_atomic_ceiling.json.  The random-address ceilings of tools/ubench.cu are beside it."""
     ach = statistics.mean(e / (k * 1e-3) / 1e9 for e, k in zip(e_pr, kms))
     out = {"achieved_gops": ach, "atom_uniform_gops": ATOM_UNIFORM_GOPS, "atom_skewed_gops": ATOM_SKEWED_GOPS,
@@ -146,7 +146,7 @@ def atomic_ceiling(e_pr, kms, args):
     try:
         with open(os.path.join(ROOT, "profiles", "r02_atomic_ceiling.json")) as f:
             c = json.load(f)[f"rmat{args.scale}_ef{args.edge_factor}_s1"]
-        out.update(peak_gops=c["mixed_r38_gops"], frac=ach / c["mixed_r38_gops"], source=c["source"])
+        out.update(peak_gops=c["product_gops"], frac=ach / c["product_gops"], source=c["source"])
     except Exception:
         out.update(peak_gops=ATOM_SKEWED_GOPS, frac=ach / ATOM_SKEWED_GOPS,
                    source="profiles/r02_ubench_sweep.md (no graph-trace ceiling for this workload)")
