@@ -35,8 +35,12 @@ struct GraphView {
 // Speculative BFS relax (Alg. 2): d = current dist[v] (R3);
 // per edge: optional read filter, atomicMin(&dist[w], d+1), push iff d+1 < old
 // (strict, R2).
+#ifndef ATOS_BFS_AGENTS
+#define ATOS_BFS_AGENTS 1
+#endif
 struct BfsApp {
   static constexpr bool kWindow = false;
+  static constexpr int kAgents = ATOS_BFS_AGENTS;  // queue agents per persistent CTA (cta_ws2.cuh)
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   uint32_t* dist;
   // near[v] = min(dist[v], 0xFFFF) as of some moment (stale values are larger,
