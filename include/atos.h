@@ -89,8 +89,8 @@ typedef struct {
                           /*   out-edges and residue < pr_defer_factor * eps is re-queued once   */
                           /*   instead of expanded (R31); 0 = off                                 */
   int32_t pr_defer_factor;
-  int32_t hub_split;      /* persistent CTA workers: split a popped vertex with > 4096 edges into  */
-                          /*   2048-edge chunk tasks (R24).  -1 = app default (BFS on, PageRank  */
+  int32_t hub_split;      /* persistent CTA workers: split a popped vertex with > 2048 edges into  */
+                          /*   1024-edge chunk tasks (R24).  -1 = app default (BFS on, PageRank  */
                           /*   off: R33), 0 = off, 1 = on                                         */
   int32_t pr_hub_check;   /* PageRank, persistent CTA workers with fp32 residues: hub targets    */
                           /*   (in-degree >= 2048) take fire-and-forget fp64 adds and are      */

@@ -569,7 +569,7 @@ constexpr int LBS_UNROLL = 8;
 // speculates on depths the hub has not yet fixed (the measured source of
 // RMAT-24 BFS overwork).
 #ifndef ATOS_CHUNK_EDGES
-#define ATOS_CHUNK_EDGES 2048
+#define ATOS_CHUNK_EDGES 1024
 #endif
 #ifndef ATOS_SPLIT_DEG
 #define ATOS_SPLIT_DEG (2 * ATOS_CHUNK_EDGES)
