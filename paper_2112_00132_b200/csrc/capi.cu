@@ -958,7 +958,7 @@ static atos_status pagerank_run(LaunchCtx& c, Residues<R> rs, double* rank, floa
     // tagged graph: fp32 sums for non-hubs, fp64 at hubs (PrInitSplitApp)
     k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rs.res, n, 0.f);
     k_zero_hubs<<<fill_blocks((n + 31) / 32, g->sms), 256, 0, c.s>>>(rs.hub, n, rs.res64, rs.r2);
-    PrInitSplitApp ia{rs.res, rs.res64, (1.0 - (double)alpha) * (double)alpha};
+    PrInitSplitApp ia{rs.res, rs.res64, rs.r2, (1.0 - (double)alpha) * (double)alpha};
     CKS((bsp_step_w<EdgeMapPolicy<PrInitSplitApp>, PrInitSplitApp, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr,
                                                                          nullptr, 256, nullptr)));
   } else {

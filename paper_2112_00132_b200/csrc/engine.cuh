@@ -166,7 +166,7 @@ struct Residues {
   // them by lane, dividing the contention on a hub's L2 line (RMAT-24 target
   // replay at the 2048 threshold: 92.7 -> 118.6 G ops/s,
   // profiles/r02_atomic_trace.md).  Every reader sums them; paths that test a
-  // crossing write replica 0 only.
+  // crossing write replica 0 only (the R4 seeding scatter spreads too).
   int64_t r2;
   __device__ __forceinline__ double hub_read(uint32_t v) const {
     double s = 0.0;

@@ -408,6 +408,7 @@ struct PrInitSplitApp {
   __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
   float* res;
   double* res64;
+  int64_t r2;  // R38: hub residue replica stride (the seeding adds spread over the replicas too)
   double c0;  // (1 - alpha) * alpha
   using Payload = double;
   using Probe = uint32_t;  // the column's hub tag
@@ -421,7 +422,7 @@ struct PrInitSplitApp {
   }
   __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
   __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
-    if (tag & TAG_HUB) red_add_hot(res64 + w, c);
+    if (tag & TAG_HUB) red_add_hot(res64 + (lane_id() & (ATOS_HUB_REPLICAS - 1u)) * r2 + w, c);
     else red_add_hot(res + w, (float)c);
     return 0;
   }
