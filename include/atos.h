@@ -95,7 +95,7 @@ typedef struct {
   int32_t pr_hub_check;   /* PageRank, persistent CTA workers with fp32 residues: hub targets    */
                           /*   (in-degree >= 2048) take fire-and-forget fp64 adds and are      */
                           /*   activated by sweeps — this many hubs checked per processed batch */
-                          /*   (R35; default 16); 0 = threshold crossing at hubs too (R34)      */
+                          /*   (R35; default 4); 0 = threshold crossing at hubs too (R34)      */
 } atos_config;
 
 /* One timeline record per batch processed by a persistent/discrete worker:

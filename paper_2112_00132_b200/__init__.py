@@ -155,7 +155,7 @@ class Config:
     pr_defer_degree: int = 0       # PR hub deferral (R31): min out-degree; 0 = off
     pr_defer_factor: int = 4       # ... defer while residue < factor * eps
     hub_split: int = -1            # hub chunk tasks (R24): -1 app default (BFS on, PR off, R33), 0 off, 1 on
-    pr_hub_check: int = 16         # PR hubs activated by sweeps, hubs checked per batch (R35); 0 = off (R34)
+    pr_hub_check: int = 4          # PR hubs activated by sweeps, hubs checked per batch (R35); 0 = off (R34)
 
     def to_c(self) -> CConfig:
         c = CConfig()

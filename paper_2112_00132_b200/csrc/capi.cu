@@ -177,7 +177,7 @@ extern "C" void atos_config_default(atos_config* c) {
   c->sink_defer = 1;
   c->pr_defer_degree = 0;
   c->pr_defer_factor = 4;
-  c->pr_hub_check = 16;
+  c->pr_hub_check = 4;
   c->hub_split = -1;
 }
 
