@@ -385,7 +385,8 @@ def run_atos(args, rank, world, local_rank):
         "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_bfs0+pagerank", "scale": args.scale,
                    "edge_factor": args.edge_factor, "n": g.n, "m": g.m, "kernel": "persistent", "worker": "cta",
                    "fetch_size": args.fetch, "pr_fetch_size": args.pr_fetch, "cta_threads": args.threads,
-                   "pr_cta_threads": args.pr_threads, "sink_defer": True,
+                   "pr_cta_threads": args.pr_threads, "sink_defer": True, "pr_hub_check": cfg_pr.pr_hub_check,
+                   "pr_hubs": "in-degree >= 2048, fp64 residues in 4 replicas, sweep-activated (R34/R35/R38)",
                    "alpha": ALPHA, "eps": EPS, "l2": "flushed (512 MB write) between steps; inputs 1.2 GB > L2",
                    "parallelism": "replicas" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": pr_ach, "peak": hbm, "unit": "GB/s", "frac": pr_ach / hbm,
