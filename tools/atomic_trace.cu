@@ -43,8 +43,13 @@ __global__ void k(const uint32_t* __restrict__ col, int64_t m, float* res, doubl
         if (w[j] & 0x80000000u) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(res64 + v), "d"(1e-7));
         else r[j] = atomicAdd(res + v, 1e-7f);
       }
-      if (MODE >= 3) {  // hub residues spread over R = 2^(MODE-2) replica arrays (replica = lane bits)
-        constexpr int R = 1 << (MODE >= 3 ? MODE - 2 : 0);
+      if (MODE == 6) {  // hubs over 4 replicas AND non-hub returning atomics over 2 fp32 replica arrays
+        const int64_t rep = (int64_t)(threadIdx.x & 3) * (int64_t)nrep;
+        if (w[j] & 0x80000000u) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(res64 + rep + v), "d"(1e-7));
+        else r[j] = atomicAdd(res + (int64_t)(threadIdx.x & 1) * nrep + v, 1e-7f);
+      }
+      if (MODE >= 3 && MODE <= 5) {  // hub residues spread over R = 2^(MODE-2) replica arrays (replica = lane bits)
+        constexpr int R = 1 << (MODE >= 3 && MODE <= 5 ? MODE - 2 : 0);
         const int64_t rep = (int64_t)(threadIdx.x & (R - 1)) * (int64_t)nrep;
         if (w[j] & 0x80000000u) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(res64 + rep + v), "d"(1e-7));
         else r[j] = atomicAdd(res + v, 1e-7f);
@@ -74,23 +79,24 @@ int main(int argc, char** argv) {
   float *res, *s;
   double* res64;
   cudaMalloc(&col, m * 4);
-  cudaMalloc(&res, n * 4);
+  cudaMalloc(&res, n * 4 * 2);  // 2 fp32 replicas (mode 6)
   cudaMalloc(&res64, n * 8 * 8);  // up to 8 replica arrays (modes 3-5)
   cudaMalloc(&s, 4);
   cudaMemcpy(col, h.data(), m * 4, cudaMemcpyHostToDevice);
-  cudaMemset(res, 0, n * 4);
+  cudaMemset(res, 0, n * 4 * 2);
   cudaMemset(res64, 0, n * 8 * 8);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const char* names[] = {"atom.add.f32 (returning) on every target", "red.add.f32 on every target",
                          "mixed: red.add.f64 at hub targets, returning atom.add.f32 elsewhere (R35)",
                          "mixed, hub residues over 2 replica arrays", "mixed, hub residues over 4 replica arrays",
-                         "mixed, hub residues over 8 replica arrays"};
+                         "mixed, hub residues over 8 replica arrays",
+                         "mixed, hubs over 4 replicas and the non-hub returning atomics over 2"};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   printf("| op | targets (edges) | ms | G ops/s |\n|---|---|---|---|\n");
-  for (int mode = 0; mode < 6; ++mode) {
+  for (int mode = 0; mode < 7; ++mode) {
     float ms = 0;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(e0);
@@ -100,6 +106,7 @@ int main(int argc, char** argv) {
       if (mode == 3) k<3><<<sms * 8, 256>>>(col, m, res, res64, s, n);
       if (mode == 4) k<4><<<sms * 8, 256>>>(col, m, res, res64, s, n);
       if (mode == 5) k<5><<<sms * 8, 256>>>(col, m, res, res64, s, n);
+      if (mode == 6) k<6><<<sms * 8, 256>>>(col, m, res, res64, s, n);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1);
