@@ -444,16 +444,23 @@ atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, ui
   }
   if (need_ring) {
     uint64_t cap = cfg.queue_capacity > 0 ? pow2_at_least((uint64_t)cfg.queue_capacity, 32) : pow2_at_least(default_cap);
-    if (cap != w.cap) {
+    // The ring is allocated for the largest capacity asked so far and each run
+    // uses its first `cap` slots (BFS and PageRank alternate 2n and 16n on one
+    // handle: no reallocation per call).  `dirty` = leading slots that may hold
+    // tags; a run clears the ones it will use, the rest stay recorded.
+    if (cap > w.ring_slots) {
       pool_free(w.ring);
       w.ring = nullptr;
       CK(pool_malloc(&w.ring, cap * sizeof(uint64_t)));
-      w.cap = cap;
+      w.ring_slots = cap;
       w.clear = cap;
+      w.dirty_rest = 0;
     } else {
       w.clear = std::min<uint64_t>(w.dirty, cap);
+      w.dirty_rest = w.dirty > cap ? w.dirty : 0;
     }
-    w.dirty = cap;  // unknown until this run finishes cleanly (finish_stats narrows it)
+    w.cap = cap;
+    w.dirty = w.ring_slots;  // unknown until this run finishes cleanly (finish_stats narrows it)
   }
   (void)n_local;
   return ATOS_OK;
@@ -820,7 +827,7 @@ static atos_status finish_stats(LaunchCtx& c, atos_stats* st, bool bsp) {
   Workspace& w = c.g->ws;
   CK(cudaEventRecord(w.ev[2], c.s));
   CKS(read_ctl(c.g, c.s));
-  if (!bsp) w.dirty = std::min<uint64_t>(w.h_ctl->tail.v, w.cap);
+  if (!bsp) w.dirty = std::max<uint64_t>(std::min<uint64_t>(w.h_ctl->tail.v, w.cap), w.dirty_rest);
   if (st) {
     float ms = 0, kms = 0;
     CK(cudaEventElapsedTime(&ms, w.ev[0], w.ev[2]));

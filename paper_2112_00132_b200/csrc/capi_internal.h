@@ -12,6 +12,8 @@ struct Workspace {
   uint64_t cap = 0;
   uint64_t dirty = 0;  // ring slots that may hold non-zero tags
   uint64_t clear = 0;  // slots the next run zeroes in its timed init (ring_reset)
+  uint64_t ring_slots = 0;  // allocated slots (>= cap, the capacity of the current run)
+  uint64_t dirty_rest = 0;  // dirty slots beyond the current run's capacity (kept for later runs)
   atos::QueueCtl* ctl = nullptr;
   atos::QueueCtl* h_ctl = nullptr;  // pinned mirror
   uint32_t* u32a = nullptr;         // BFS dist / GC pend

@@ -894,7 +894,7 @@ static atos_status part_call(LaunchCtx& c, int app, int64_t src, float alpha, fl
   }
   CK(cudaEventRecord(w.ev[2], c.s));
   CKS(read_ctl(g, c.s));
-  w.dirty = std::min<uint64_t>(w.h_ctl->tail.v, w.cap);
+  w.dirty = std::max<uint64_t>(std::min<uint64_t>(w.h_ctl->tail.v, w.cap), w.dirty_rest);
   if (st) {
     float ms = 0, kms = 0;
     CK(cudaEventElapsedTime(&ms, w.ev[0], w.ev[2]));

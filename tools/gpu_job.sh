@@ -1,2 +1,4 @@
 # ad-hoc GPU job (overwritten per experiment; the committed copy is the last one run)
-timeout 600 python tools/atomic_trace.py --scale 24 --hub 2048 > gpurun_out/atrace4.md 2>&1; echo at=$?; cat gpurun_out/atrace4.md
+python -c "import __graft_entry__ as e; e.build()" > gpurun_out/build.log 2>&1
+timeout 1800 python -m pytest tests -q -m gpu -x --timeout 600 > gpurun_out/pytest.log 2>&1; echo pytest_rc=$?; tail -2 gpurun_out/pytest.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; echo bench_rc=$?; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['pagerank']['kernel_ms'], d['pagerank']['ms'], d['bfs']['kernel_ms'], d['bfs']['ms'], d['bfs']['gteps'], d['e2e']['value'])"
