@@ -579,10 +579,11 @@ static atos_status run_persistent_w(LaunchCtx& c, const App& app, const Queue& q
   const int F = c.cfg.fetch_size, T = clamp_threads(W, F, c.cfg.cta_threads, P::kWarpSpecialised);
   Queue qq = q;
   // R24 hub chunk tasks: only if some vertex is a hub; the table has one
-  // 16-B entry per ring slot (device.cuh, Chunk), so it cannot overflow
+  // 16-B entry per ring slot (device.cuh, Chunk; indexed by pos & mask), so it
+  // cannot overflow.  Like the ring it is kept at the largest capacity seen.
   if (W == W_CTA && P::kSplit && c.split && c.g->max_degree > SPLIT_DEG) {
     Workspace& w = c.g->ws;
-    if (w.chunk_cap != w.cap) {
+    if (w.chunk_cap < w.cap) {
       pool_free(w.chunks);
       w.chunks = nullptr;
       w.chunk_cap = 0;
@@ -815,6 +816,11 @@ static atos_status bsp_read_count(LaunchCtx& c, unsigned long long* dcount, uint
 }
 
 static int fill_blocks(int64_t n, int sms) { return grid_for(n, 256, sms); }
+// k_pr_seed: 8 resident CTAs per SM, at most one per merge-path tile
+static int seed_blocks(atos_graph g) {
+  const int64_t tiles = (g->n + g->m + SEED_D - 1) / SEED_D;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)g->sms * 8));
+}
 
 // Output copy: host or device destination (UVA).
 static atos_status copy_out(void* dst, const void* src, size_t bytes, cudaStream_t s) {
@@ -959,21 +965,17 @@ static atos_status pagerank_run(LaunchCtx& c, Residues<R> rs, double* rank, floa
   // growing sum round with correlated errors (measured: RMAT-27's hub 4.8e-4 of max x* low)
   const bool f32 = !std::is_same<R, double>::value;
   k_ctl_init<<<1, 1, 0, c.s>>>(w.ctl, bsp ? 0 : (uint64_t)n, w.ring, -1);
-  LaunchCtx ci = c;
-  ci.cfg.worker = ATOS_WORKER_CTA;
   if constexpr (std::is_same<R, float>::value) {
-    // tagged graph: fp32 sums for non-hubs, fp64 at hubs (PrInitSplitApp)
+    // tagged graph: fp32 sums for non-hubs, fp64 at hubs (k_pr_seed<true>)
     k_fill<float><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(rs.res, n, 0.f);
     k_zero_hubs<<<fill_blocks((n + 31) / 32, g->sms), 256, 0, c.s>>>(rs.hub, n, rs.res64, rs.r2);
-    PrInitSplitApp ia{rs.res, rs.res64, rs.r2, (1.0 - (double)alpha) * (double)alpha};
-    CKS((bsp_step_w<EdgeMapPolicy<PrInitSplitApp>, PrInitSplitApp, W_CTA>(ci, ia, nullptr, (uint64_t)n, nullptr,
-                                                                         nullptr, 256, nullptr)));
+    k_pr_seed<true><<<seed_blocks(g), SEED_T, 0, c.s>>>(g->d_off, (const uint32_t*)g->d_col, n, g->m, rs.res, rs.res64, rs.r2,
+                                                        (1.0 - (double)alpha) * (double)alpha);
   } else {
     double* acc = w.f64b;  // every residue fp64: the sums are the residues
     k_fill<double><<<fill_blocks(n, g->sms), 256, 0, c.s>>>(acc, n, 0.0);
-    PrInitAppT<double> ia{acc, (1.0 - (double)alpha) * (double)alpha};
-    CKS((bsp_step_w<EdgeMapPolicy<PrInitAppT<double>>, PrInitAppT<double>, W_CTA>(ci, ia, nullptr, (uint64_t)n,
-                                                                                 nullptr, nullptr, 256, nullptr)));
+    k_pr_seed<false><<<seed_blocks(g), SEED_T, 0, c.s>>>(g->d_off, (const uint32_t*)g->d_col, n, g->m, nullptr, acc, 0,
+                                                         (1.0 - (double)alpha) * (double)alpha);
   }
   if (!bsp) k_ring_prefill<<<fill_blocks(n, g->sms), 256, 0, c.s>>>(w.ring, n, 0u);
   // R29: sink deferral for the threshold-activated queue strategies

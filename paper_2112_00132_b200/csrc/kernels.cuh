@@ -370,67 +370,87 @@ __global__ void k_bfs_init(uint32_t* dist, uint32_t* done, uint16_t* near, int64
   }
 }
 
-// PR residue seeding (reading R4 of Alg. 3 lines 5-7): the edge-map of an
-// app that pushes c = (1-a) a / deg(v) to every out-neighbour, no activation.
-template <class R>
-struct PrInitAppT {
-  static constexpr bool kWindow = false;
-  __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
-  R* res;
-  R c0;  // (1 - alpha) * alpha
-  using Payload = R;
-  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1, Payload& p) const {
-    e0 = ld_nc_s64(g.off + v);
-    e1 = ld_nc_s64(g.off + v + 1);
-    if (e1 == e0) return false;
-    p = c0 / (R)(e1 - e0);
-    return true;
+// PR residue seeding (reading R4 of Alg. 3 lines 5-7): every edge v->w adds
+// c = (1-a) a / deg(v) to r(w), no activation.  With R34's storage the add to a
+// hub target (column HUB_TAG) accumulates in fp64 (red.add.f64 into the hub's
+// replica lane & 3, R38 — hundreds of thousands of equal adds, R30), every
+// other target in its fp32 residue directly (< 2048 adds, R34's argument); with
+// all-fp64 residues (!SPLIT) every add is fp64.
+//
+// One flat pass over the edge array rather than an edge map over the
+// all-vertex frontier: the (vertex, edge) sequence — vertex i's end offset
+// off[i+1] merged with the edge indices 0..m-1 — is cut into tiles of SEED_D
+// items along the merge path, so every tile holds at most SEED_D vertices +
+// edges whatever the degree mix (runs of empty vertices, out-degree hubs).
+// Each CTA walks a contiguous run of tiles, locating only its first tile in
+// HBM and every later one inside the offsets it has staged in shared memory.
+// Edges of a tile go to threads round-robin (coalesced column reads); an
+// edge's source is the last staged vertex whose offset is <= the edge index.
+// Every edge issues one non-returning atomic, so the pass runs at the L2
+// atomic rate of the graph's own targets (profiles/r02_seed.md).
+constexpr int SEED_T = 256, SEED_D = 2048;
+__device__ __forceinline__ int64_t seed_path(const int64_t* off, int64_t n, int64_t m, int64_t diag) {
+  // vertices fully consumed at merge-path diagonal `diag` (Merrill & Garland's CSR merge path)
+  int64_t lo = diag > m ? diag - m : 0, hi = diag < n ? diag : n;
+  while (lo < hi) {
+    const int64_t p = (lo + hi) >> 1;
+    if (off[p + 1] <= diag - p - 1) lo = p + 1;
+    else hi = p;
   }
-  __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t) const {
-    atomicAdd(res + w, c);
-    return false;
+  return lo;
+}
+template <bool SPLIT>
+__global__ void __launch_bounds__(SEED_T) k_pr_seed(const int64_t* __restrict__ off, const uint32_t* __restrict__ col,
+                                                    int64_t n, int64_t m, float* res, double* res64, int64_t r2,
+                                                    double c0) {
+  __shared__ int64_t s_off[SEED_D + 2];
+  __shared__ int64_t s_end[2];
+  const int64_t tiles = (n + m + SEED_D - 1) / SEED_D;
+  const int64_t t0 = tiles * blockIdx.x / gridDim.x, t1 = tiles * (blockIdx.x + 1) / gridDim.x;
+  if (t0 >= t1) return;
+  int64_t i0 = seed_path(off, n, m, t0 * SEED_D);  // first vertex of the CTA's run
+  int64_t j0 = t0 * SEED_D - i0;                   // first edge
+  const uint32_t rep = lane_id() & (ATOS_HUB_REPLICAS - 1u);
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t nv = n - i0 < SEED_D + 1 ? n - i0 + 1 : SEED_D + 2;  // staged entries off[i0 ..]
+    for (int k = threadIdx.x; k < nv; k += SEED_T) s_off[k] = __ldg(off + i0 + k);
+    __syncthreads();
+    if (threadIdx.x == 0) {  // the tile's end point, by the same merge-path search over the staged offsets
+      const int64_t d = (t + 1) * SEED_D < n + m ? SEED_D : n + m - t * SEED_D;
+      int64_t lo = d > m - j0 ? d - (m - j0) : 0, hi = d < n - i0 ? d : n - i0;
+      while (lo < hi) {
+        const int64_t p = (lo + hi) >> 1;
+        if (s_off[p + 1] <= j0 + (d - p - 1)) lo = p + 1;
+        else hi = p;
+      }
+      s_end[0] = i0 + lo;
+      s_end[1] = j0 + d - lo;
+    }
+    __syncthreads();
+    const int64_t i1 = s_end[0], j1 = s_end[1];
+    const int last = (int)(i1 - i0 < nv - 2 ? i1 - i0 : nv - 2);  // last staged vertex that can own an edge
+    for (int64_t e = j0 + threadIdx.x; e < j1; e += SEED_T) {
+      int lo = 0, hi = last;  // largest k with s_off[k] <= e
+      while (lo < hi) {
+        const int p = (lo + hi + 1) >> 1;
+        if (s_off[p] <= e) lo = p;
+        else hi = p - 1;
+      }
+      const double c = c0 / (double)(s_off[lo + 1] - s_off[lo]);
+      const uint32_t raw = __ldg(col + e), w = raw & VID_MASK;
+      if (SPLIT) {
+        if ((raw >> TAG_SHIFT) & TAG_HUB) red_add_hot(res64 + rep * r2 + w, c);
+        else red_add_hot(res + w, (float)c);
+      } else {
+        red_add_hot(res64 + w, c);
+      }
+    }
+    __syncthreads();  // s_off / s_end are restaged
+    i0 = i1;
+    j0 = j1;
   }
-  using Probe = int;
-  __device__ __forceinline__ Probe probe(uint32_t, uint32_t) const { return 0; }
-  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe) const { return edge(c, w, 0); }
-  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
-  using Raw = int;
-  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe) const { atomicAdd(res + w, c); return 0; }
-  __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
-};
+}
 
-// R4 seeding with R34's storage: the push to a hub target (column HUB_TAG)
-// accumulates in fp64 (res64, red.add.f64 — hundreds of thousands of equal
-// adds, R30), every other target in its fp32 residue directly (< 512 adds,
-// R34's argument), so no fp64 staging array and no rounding pass.
-struct PrInitSplitApp {
-  static constexpr bool kWindow = false;
-  __device__ __forceinline__ uint32_t item_of(uint32_t w) const { return w; }
-  float* res;
-  double* res64;
-  int64_t r2;  // R38: hub residue replica stride (the seeding adds spread over the replicas too)
-  double c0;  // (1 - alpha) * alpha
-  using Payload = double;
-  using Probe = uint32_t;  // the column's hub tag
-  using Raw = int;
-  __device__ __forceinline__ bool begin(uint32_t v, const GraphView& g, int64_t& e0, int64_t& e1, Payload& p) const {
-    e0 = ld_nc_s64(g.off + v);
-    e1 = ld_nc_s64(g.off + v + 1);
-    if (e1 == e0) return false;
-    p = c0 / (double)(e1 - e0);
-    return true;
-  }
-  __device__ __forceinline__ Probe probe(uint32_t, uint32_t tag) const { return tag; }
-  __device__ __forceinline__ Raw issue(Payload c, uint32_t w, Probe tag) const {
-    if (tag & TAG_HUB) red_add_hot(res64 + (lane_id() & (ATOS_HUB_REPLICAS - 1u)) * r2 + w, c);
-    else red_add_hot(res + w, (float)c);
-    return 0;
-  }
-  __device__ __forceinline__ bool decide(Payload, uint32_t, Probe, Raw) const { return false; }
-  __device__ __forceinline__ bool commit(Payload c, uint32_t w, Probe t) const { return decide(c, w, t, issue(c, w, t)); }
-  __device__ __forceinline__ bool edge(Payload c, uint32_t w, uint32_t t) const { return commit(c, w, t); }
-  __device__ __forceinline__ bool chunk_current(uint32_t, Payload) const { return true; }
-};
 // zero the fp64 residue of every hub (bit set in the hub bitmap)
 __global__ void k_zero_hubs(const uint32_t* bits, int64_t n, double* res64, int64_t r2) {
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < (n + 31) / 32; w += (int64_t)gridDim.x * blockDim.x) {
