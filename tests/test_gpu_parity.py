@@ -566,6 +566,38 @@ def test_pagerank_window_activation(atos, gname, check_size):
     assert st["max_residue"] <= 1e-6
 
 
+def seed_tiles_graph():
+    """Merge-path tile edge cases for the R4 seeding pass (k_pr_seed, 2,048
+    vertices + edges per tile): a 5,000-vertex run of isolated vertices, one
+    vertex of out-degree 7,000 spanning several tiles, another isolated run,
+    a 3,000-way fan-in onto the last vertex (in-degree >= 2048: a hub, fp64
+    seeding into its replicas) and a seeded random tail."""
+    n = 20000
+    rng = np.random.default_rng(7)
+    e = [(5000, int(t)) for t in rng.choice(np.arange(5001, n), 7000, replace=False)]
+    e += [(int(v), n - 1) for v in range(12000, 15000)]
+    tail = rng.integers(15000, n, size=(20000, 2))
+    e += [(int(a), int(b)) for a, b in tail if a != b]
+    return gg.from_edges(n, e)
+
+
+@pytest.mark.parametrize("gname", ["tiles", "cycle1024", "cycle2048", "K9", "empty5"])
+@pytest.mark.parametrize("fp64", [False, True])
+def test_pagerank_seeding_tiles(atos, gname, fp64):
+    """R4 seeding over merge-path tiles: graphs whose n + m is below one tile,
+    exactly one or two tiles (directed cycles: n + m = 2n), and a graph whose
+    vertex runs and out-degree hub cross tile boundaries.  Both storages:
+    fp32 with fp64 hubs (tagged) and all-fp64 residues."""
+    g = {"tiles": seed_tiles_graph, "cycle1024": lambda: gg.cycle(1024, directed=True),
+         "cycle2048": lambda: gg.cycle(2048, directed=True), "K9": lambda: G("K9"),
+         "empty5": lambda: G("empty5")}[gname]()
+    x = oracle.pagerank(g, 0.85)[0]
+    r, st = atos.pagerank(atos.Graph.from_csr(g), 0.85, 1e-6, pr_residue_fp64=fp64, timeout_s=60)
+    assert np.max(np.abs(r.astype(np.float64) - x)) / x.max() <= PR_TOL
+    assert st["max_residue"] <= 1e-6
+    assert np.all(r <= x * ONE_SIDED + 1e-6)
+
+
 def test_pagerank_cta_threads_floor(atos):
     # persistent CTA PageRank runs two queue-agent warps per CTA: at least one worker warp more
     with pytest.raises(atos.AtosError) as e:

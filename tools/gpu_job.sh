@@ -1,8 +1,5 @@
 # ad-hoc GPU job (overwritten per experiment; the committed copy is the last one run)
 python -c "import __graft_entry__ as e; e.build()" > gpurun_out/build.log 2>&1
-for v in old new; do
-  if [ $v = old ]; then export ATOS_LIB=paper_2112_00132_b200/variants/libatos_old.so; else unset ATOS_LIB; fi
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_pr_seed|PrInitSplit" --csv --log-file gpurun_out/seed_$v.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_$v.log 2>&1; echo ncu_$v=$?
-done
-unset ATOS_LIB
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pr_seed" -c 1 -o gpurun_out/seed_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo full=$?
+timeout 1800 python -m pytest tests -q -m gpu -x --timeout 600 > gpurun_out/pytest.log 2>&1; echo pytest_rc=$?; tail -2 gpurun_out/pytest.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; echo bench_rc=$?; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['pagerank']['kernel_ms'], d['pagerank']['ms'], d['bfs']['kernel_ms'], d['bfs']['ms'], d['bfs']['gteps'], d['e2e']['value'])"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu.log 2>&1; echo ncu_rc=$?
