@@ -223,13 +223,27 @@ static atos_status check_config(const atos_config* c) {
 
 // ------------------------------------------------------------------ graph
 __global__ void k_validate(const int64_t* off, const int32_t* col, int64_t n, int64_t m, int64_t col_bound,
-                           unsigned int* bad) {
+                           unsigned int* bad, bool cols) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = tid; v < n; v += stride)
     if (off[v + 1] < off[v]) atomicOr(bad, 1u);
-  for (int64_t e = tid; e < m; e += stride)
+  for (int64_t e = tid; cols && e < m; e += stride)
     if (col[e] < 0 || (int64_t)col[e] >= col_bound) atomicOr(bad, 2u);
   if (tid == 0 && (off[0] != 0 || off[n] != m)) atomicOr(bad, 4u);
+}
+// One pass over a freshly uploaded chunk of columns [e0, e1): the range check
+// of ATOS_GRAPH_VALIDATE (bad |= 2) and/or the in-degree count of R34's hub
+// tagging (in-range targets only; a bad column fails the create anyway).
+__global__ void k_col_pass(const int32_t* col, int64_t e0, int64_t e1, int64_t n, int64_t col_bound,
+                           uint32_t* indeg, unsigned int* bad) {
+  bool ok = true;
+  for (int64_t e = e0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = col[e];
+    const bool in = c >= 0 && (int64_t)c < col_bound;
+    ok &= in;
+    if (indeg && in && (int64_t)c < n) atomicAdd(indeg + c, 1u);
+  }
+  if (bad && !ok) atomicOr(bad, 2u);
 }
 __global__ void k_max_degree(const int64_t* off, int64_t n, unsigned long long* out) {
   unsigned long long m = 0;
@@ -254,6 +268,56 @@ static atos_status device_sms(int* sms) {
   return ATOS_OK;
 }
 
+// Upload of a library-owned CSR copy, pipelined: the offsets, then the
+// columns in chunks on one stream while a second stream runs k_col_pass over
+// every chunk that has landed (the VALIDATE range check and the in-degree count
+// R34's hub tags need), so both hide under the copy.  A whole-graph copy
+// (col_bound == n, m > 0) leaves the in-degrees in g->d_indeg for the tagging.
+static atos_status upload_csr(atos_graph g, const int64_t* off, const int32_t* col, bool dev_ptrs,
+                              int64_t col_bound, bool validate) {
+  const int64_t n = g->n, m = g->m;
+  const cudaMemcpyKind kind = dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault;
+  const bool count = col_bound == n && m > 0;
+  CK(cudaMalloc(&g->d_scratch, 256));
+  CK(cudaMemset(g->d_scratch, 0, 256));
+  if (count) {
+    CK(pool_malloc(&g->d_indeg, (size_t)n * sizeof(uint32_t)));
+    CK(cudaMemset(g->d_indeg, 0, (size_t)n * sizeof(uint32_t)));
+  }
+  CK(cudaDeviceSynchronize());  // the allocations and zeroing above ran on the legacy stream
+  cudaStream_t cp = nullptr, pass = nullptr;
+  cudaEvent_t landed = nullptr;
+  auto done = [&](cudaError_t e) {
+    if (cp) cudaStreamSynchronize(cp);
+    if (pass) cudaStreamSynchronize(pass);
+    if (landed) cudaEventDestroy(landed);
+    if (cp) cudaStreamDestroy(cp);
+    if (pass) cudaStreamDestroy(pass);
+    if (e != cudaSuccess) return atos_set_error(ATOS_ERR_CUDA, "CSR upload: %s", cudaGetErrorString(e));
+    return ATOS_OK;
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pass, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&landed, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_off, off, (size_t)(n + 1) * sizeof(int64_t), kind, cp);
+  unsigned int* bad = validate ? reinterpret_cast<unsigned int*>(g->d_scratch) : nullptr;
+  uint32_t* indeg = count ? g->d_indeg : nullptr;
+  const int64_t chunk = (int64_t)1 << 25;  // 128 MB of columns
+  for (int64_t e0 = 0; e == cudaSuccess && e0 < m; e0 += chunk) {
+    const int64_t e1 = std::min(m, e0 + chunk);
+    e = cudaMemcpyAsync(g->d_col + e0, col + e0, (size_t)(e1 - e0) * sizeof(int32_t), kind, cp);
+    if (e == cudaSuccess && (bad || indeg)) {
+      e = cudaEventRecord(landed, cp);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(pass, landed, 0);
+      if (e == cudaSuccess) {
+        k_col_pass<<<grid_for(e1 - e0, 256, g->sms), 256, 0, pass>>>(g->d_col, e0, e1, n, col_bound, indeg, bad);
+        e = cudaGetLastError();
+      }
+    }
+  }
+  return done(e);
+}
+
 atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* col, int64_t n, int64_t m,
                               uint32_t flags, int64_t col_bound) {
   if (col_bound < 0) col_bound = n;
@@ -275,8 +339,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     CK(pool_malloc(&g->d_col, (size_t)g->col_cap * sizeof(int32_t)));
     CK(cudaMemset(g->d_col + m, 0, (size_t)(g->col_cap - m) * sizeof(int32_t)));  // the pad only
     g->owned = true;
-    CK(cudaMemcpy(g->d_off, off, (size_t)(n + 1) * sizeof(int64_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
-    if (m) CK(cudaMemcpy(g->d_col, col, (size_t)m * sizeof(int32_t), dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault));
+    CKS(upload_csr(g, off, col, dev_ptrs, col_bound, (flags & ATOS_GRAPH_VALIDATE) != 0));
   }
   // L2 set-aside for evict_last (persisting) lines: the per-vertex state the
   // edge loop hits at random (BFS dist, PR residue) is accessed with an
@@ -292,11 +355,14 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
       (void)cudaGetLastError();
     }
   }
-  CK(cudaMalloc(&g->d_scratch, 256));
-  CK(cudaMemset(g->d_scratch, 0, 256));
+  if (!g->d_scratch) {
+    CK(cudaMalloc(&g->d_scratch, 256));
+    CK(cudaMemset(g->d_scratch, 0, 256));
+  }
   if (flags & ATOS_GRAPH_VALIDATE) {
     unsigned int* bad = reinterpret_cast<unsigned int*>(g->d_scratch);
-    k_validate<<<grid_for(std::max(n, m), 256, g->sms), 256>>>(g->d_off, g->d_col, n, m, col_bound, bad);
+    // owned copies had their columns checked chunk by chunk during the upload (k_col_pass)
+    k_validate<<<grid_for(std::max(n, m), 256, g->sms), 256>>>(g->d_off, g->d_col, n, m, col_bound, bad, !g->owned);
     unsigned int hbad = 0;
     CK(cudaMemcpy(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost));
     if (hbad)
@@ -316,10 +382,8 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
   // bitmap.  (Borrowed columns are the caller's and partitioned graphs only
   // know local edges: neither is tagged, and PageRank keeps fp64 residues.)
   if (g->owned && col_bound == n && m > 0) {
-    uint32_t* indeg = nullptr;
-    CK(pool_malloc(&indeg, (size_t)n * sizeof(uint32_t)));
-    CK(cudaMemset(indeg, 0, (size_t)n * sizeof(uint32_t)));
-    k_in_degree<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, indeg);
+    uint32_t* indeg = g->d_indeg;  // counted during the upload (upload_csr)
+    g->d_indeg = nullptr;
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g->d_scratch) + 4;
     CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
     CK(pool_malloc(&g->d_hub, (size_t)((n + 31) / 32) * sizeof(uint32_t)));
@@ -327,7 +391,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     unsigned long long hubs = 0;
     CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
     g->num_hubs = (int64_t)hubs;
-    k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, indeg, HUB_IN_DEG, g->d_sink);
+    k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, g->d_hub, g->d_sink);
     if (hubs) {  // R35: the hubs a PageRank sweep may activate (dangling hubs are absorbed at the end, R29)
       CK(pool_malloc(&g->d_hub_list, (size_t)hubs * sizeof(uint32_t)));
       CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
@@ -359,6 +423,7 @@ static void graph_free(atos_graph g) {
   cudaFree(g->d_scratch);
   pool_free(g->d_sink);
   pool_free(g->d_hub);
+  pool_free(g->d_indeg);
   pool_free(g->d_hub_list);
   Workspace& w = g->ws;
   pool_free(w.ring);

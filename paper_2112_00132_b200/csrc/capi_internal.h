@@ -50,6 +50,7 @@ struct atos_graph_s {
   int32_t* d_col = nullptr;
   int64_t col_cap = 0;  // readable elements of d_col
   uint32_t* d_sink = nullptr;  // bit v = (deg(v) == 0), built at create (R29)
+  uint32_t* d_indeg = nullptr;  // in-degrees counted during the upload, freed after tagging
   uint32_t* d_hub = nullptr;   // bit v = in-degree >= HUB_IN_DEG; columns carry HUB_TAG (R34); nullptr = untagged
   int64_t num_hubs = 0;
   uint32_t* d_hub_list = nullptr;  // hub vertex ids with out-degree > 0 (R35 sweep activation)

@@ -493,15 +493,13 @@ __global__ void k_sink_bitmap(const int64_t* off, int64_t n, uint32_t* bits) {
 // Column tagging (R34, R37), at graph create: in-degree histogram, then bit
 // 31 of every column entry whose target has in-degree >= thr, bit 30 if the
 // target is dangling (the sink bitmap), and the hub bitmap.
-__global__ void k_in_degree(const int32_t* col, int64_t m, int64_t n, uint32_t* indeg) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(indeg + ATOS_CHK((uint32_t)col[e] & VID_MASK, (uint32_t)n), 1u);
-}
-__global__ void k_tag_hubs(int32_t* col, int64_t m, int64_t n, const uint32_t* indeg, uint32_t thr,
-                           const uint32_t* sink) {
+// tags from the two 2-MB bitmaps (hub: in-degree >= HUB_IN_DEG, sink: out-degree 0),
+// which stay in L2/L1, rather than the 64-MB in-degree array
+__global__ void k_tag_hubs(int32_t* col, int64_t m, int64_t n, const uint32_t* hub, const uint32_t* sink) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t w = ATOS_CHK((uint32_t)col[e] & VID_MASK, (uint32_t)n);
-    col[e] = (int32_t)(w | (indeg[w] >= thr ? HUB_TAG : 0u) | (((sink[w >> 5] >> (w & 31)) & 1u) ? SINK_TAG : 0u));
+    const uint32_t h = (__ldg(hub + (w >> 5)) >> (w & 31)) & 1u, k = (__ldg(sink + (w >> 5)) >> (w & 31)) & 1u;
+    col[e] = (int32_t)(w | (h ? HUB_TAG : 0u) | (k ? SINK_TAG : 0u));
   }
 }
 __global__ void k_hub_bitmap(const uint32_t* indeg, int64_t n, uint32_t thr, uint32_t* bits,
