@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -391,7 +392,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     unsigned long long hubs = 0;
     CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
     g->num_hubs = (int64_t)hubs;
-    k_tag_hubs<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, m, n, g->d_hub, g->d_sink);
+    k_tag_hubs<<<grid_for((m + 3) / 4, 256, g->sms), 256>>>(g->d_col, m, n, g->d_hub, g->d_sink);
     if (hubs) {  // R35: the hubs a PageRank sweep may activate (dangling hubs are absorbed at the end, R29)
       CK(pool_malloc(&g->d_hub_list, (size_t)hubs * sizeof(uint32_t)));
       CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
@@ -407,6 +408,65 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return check_failures();
+}
+
+// Per-run control blocks (device QueueCtl, its pinned host mirror, the BSP
+// counter, the timing events) are recycled across graph handles: a handle's
+// first call would otherwise pay cudaMalloc + cudaMallocHost + event creation,
+// and its destroy the matching frees (measured: ~6 ms of the first BFS on a
+// fresh handle in the e2e loop).  Keyed by device; at most kCtlCache kept.
+struct CtlBlock {
+  int device;
+  QueueCtl* ctl;
+  QueueCtl* h_ctl;
+  unsigned long long* fcount;
+  cudaEvent_t ev[4];
+};
+static std::mutex g_ctl_mu;
+static std::vector<CtlBlock> g_ctl_cache;
+constexpr size_t kCtlCache = 16;
+
+static atos_status ctl_acquire(Workspace& w, int device) {
+  {
+    std::lock_guard<std::mutex> lk(g_ctl_mu);
+    for (size_t i = 0; i < g_ctl_cache.size(); ++i)
+      if (g_ctl_cache[i].device == device) {
+        const CtlBlock b = g_ctl_cache[i];
+        g_ctl_cache.erase(g_ctl_cache.begin() + (std::ptrdiff_t)i);
+        w.ctl = b.ctl;
+        w.h_ctl = b.h_ctl;
+        w.fcount = b.fcount;
+        for (int k = 0; k < 4; ++k) w.ev[k] = b.ev[k];
+        return ATOS_OK;
+      }
+  }
+  CK(cudaMalloc(&w.ctl, sizeof(QueueCtl)));
+  CK(cudaMallocHost(&w.h_ctl, sizeof(QueueCtl)));
+  for (auto& e : w.ev) CK(cudaEventCreate(&e));
+  CK(cudaMalloc(&w.fcount, 4 * sizeof(unsigned long long)));
+  return ATOS_OK;
+}
+
+static void ctl_release(Workspace& w, int device) {
+  if (!w.ctl || !w.h_ctl || !w.fcount || !w.ev[0] || !w.ev[1] || !w.ev[2] || !w.ev[3]) {
+    cudaFree(w.ctl);
+    cudaFree(w.fcount);
+    if (w.h_ctl) cudaFreeHost(w.h_ctl);
+    for (auto& e : w.ev)
+      if (e) cudaEventDestroy(e);
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_ctl_mu);
+    if (g_ctl_cache.size() < kCtlCache) {
+      g_ctl_cache.push_back(CtlBlock{device, w.ctl, w.h_ctl, w.fcount, {w.ev[0], w.ev[1], w.ev[2], w.ev[3]}});
+      return;
+    }
+  }
+  cudaFree(w.ctl);
+  cudaFree(w.fcount);
+  cudaFreeHost(w.h_ctl);
+  for (auto& e : w.ev) cudaEventDestroy(e);
 }
 
 static void graph_free(atos_graph g) {
@@ -427,7 +487,6 @@ static void graph_free(atos_graph g) {
   pool_free(g->d_hub_list);
   Workspace& w = g->ws;
   pool_free(w.ring);
-  cudaFree(w.ctl);
   pool_free(w.u32a);
   pool_free(w.u32b);
   pool_free(w.u16a);
@@ -437,13 +496,10 @@ static void graph_free(atos_graph g) {
   pool_free(w.f64b);
   pool_free(w.front[0]);
   pool_free(w.front[1]);
-  cudaFree(w.fcount);
   pool_free(w.chunks);
   cudaFree(w.devround);
-  if (w.h_ctl) cudaFreeHost(w.h_ctl);
-  for (auto& e : w.ev)
-    if (e) cudaEventDestroy(e);
   dist_free(g);
+  ctl_release(w, g->device);
   delete g;
 }
 
@@ -501,12 +557,7 @@ static uint64_t pow2_at_least(uint64_t x, uint64_t floor_cap = 1024) {
 atos_status ws_prepare(atos_graph g, const atos_config& cfg, int64_t n_local, uint64_t default_cap, bool need_ring,
                        cudaStream_t s) {
   Workspace& w = g->ws;
-  if (!w.ctl) {
-    CK(cudaMalloc(&w.ctl, sizeof(QueueCtl)));
-    CK(cudaMallocHost(&w.h_ctl, sizeof(QueueCtl)));
-    for (auto& e : w.ev) CK(cudaEventCreate(&e));
-    CK(cudaMalloc(&w.fcount, 4 * sizeof(unsigned long long)));
-  }
+  if (!w.ctl) CKS(ctl_acquire(w, g->device));
   if (need_ring) {
     uint64_t cap = cfg.queue_capacity > 0 ? pow2_at_least((uint64_t)cfg.queue_capacity, 32) : pow2_at_least(default_cap);
     // The ring is allocated for the largest capacity asked so far and each run

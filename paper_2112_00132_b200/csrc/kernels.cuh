@@ -494,13 +494,27 @@ __global__ void k_sink_bitmap(const int64_t* off, int64_t n, uint32_t* bits) {
 // 31 of every column entry whose target has in-degree >= thr, bit 30 if the
 // target is dangling (the sink bitmap), and the hub bitmap.
 // tags from the two 2-MB bitmaps (hub: in-degree >= HUB_IN_DEG, sink: out-degree 0),
-// which stay in L2/L1, rather than the 64-MB in-degree array
+// which stay in L2, rather than the 64-MB in-degree array; four columns per
+// thread (one 16-B load; col is 16-B aligned and padded, capi.cu) so eight
+// independent bitmap loads are in flight per thread
+__device__ __forceinline__ uint32_t tag_of(uint32_t raw, int64_t n, const uint32_t* hub, const uint32_t* sink) {
+  const uint32_t w = ATOS_CHK(raw & VID_MASK, (uint32_t)n);
+  const uint32_t h = (__ldg(hub + (w >> 5)) >> (w & 31)) & 1u, k = (__ldg(sink + (w >> 5)) >> (w & 31)) & 1u;
+  return w | (h ? HUB_TAG : 0u) | (k ? SINK_TAG : 0u);
+}
 __global__ void k_tag_hubs(int32_t* col, int64_t m, int64_t n, const uint32_t* hub, const uint32_t* sink) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t w = ATOS_CHK((uint32_t)col[e] & VID_MASK, (uint32_t)n);
-    const uint32_t h = (__ldg(hub + (w >> 5)) >> (w & 31)) & 1u, k = (__ldg(sink + (w >> 5)) >> (w & 31)) & 1u;
-    col[e] = (int32_t)(w | (h ? HUB_TAG : 0u) | (k ? SINK_TAG : 0u));
+  const int64_t q = m >> 2;
+  uint4* c4 = reinterpret_cast<uint4*>(col);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 v = c4[i];
+    v.x = tag_of(v.x, n, hub, sink);
+    v.y = tag_of(v.y, n, hub, sink);
+    v.z = tag_of(v.z, n, hub, sink);
+    v.w = tag_of(v.w, n, hub, sink);
+    c4[i] = v;
   }
+  const int64_t e = 4 * q + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < m) col[e] = (int32_t)tag_of((uint32_t)col[e], n, hub, sink);
 }
 __global__ void k_hub_bitmap(const uint32_t* indeg, int64_t n, uint32_t thr, uint32_t* bits,
                              unsigned long long* count) {
