@@ -40,6 +40,7 @@ def main():
             tb = time.perf_counter()
             print("  bfs first: wall %.1f ms, device %.2f ms (kernel %.2f); again: wall %.1f ms, device %.2f ms (kernel %.2f)"
                   % ((t2 - t1) * 1e3, s1["ms"], s1["kernel_ms"], (tb - t2) * 1e3, s2["ms"], s2["kernel_ms"]), flush=True)
+            t1 += time.perf_counter() - t2  # the bfs column keeps the first call only
             t2 = time.perf_counter()
         atos.pagerank(G, 0.85, 1e-6, cp, out=rk.numpy())
         t3 = time.perf_counter()
