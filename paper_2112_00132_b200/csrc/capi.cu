@@ -392,7 +392,9 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     unsigned long long hubs = 0;
     CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
     g->num_hubs = (int64_t)hubs;
-    k_tag_hubs<<<grid_for((m + 3) / 4, 256, g->sms), 256>>>(g->d_col, m, n, g->d_hub, g->d_sink);
+    // the in-degree array (n words) is dead once the hub bitmap exists: it holds the interleaved tag map
+    k_tag_map<<<grid_for((n + 15) / 16, 256, g->sms), 256>>>(g->d_hub, g->d_sink, n, indeg);
+    k_tag_hubs<<<grid_for((m + 3) / 4, 256, g->sms), 256>>>(g->d_col, m, n, indeg);
     if (hubs) {  // R35: the hubs a PageRank sweep may activate (dangling hubs are absorbed at the end, R29)
       CK(pool_malloc(&g->d_hub_list, (size_t)hubs * sizeof(uint32_t)));
       CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
