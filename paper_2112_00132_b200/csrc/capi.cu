@@ -269,11 +269,29 @@ static atos_status device_sms(int* sms) {
   return ATOS_OK;
 }
 
-// Upload of a library-owned CSR copy, pipelined: the offsets, then the
-// columns in chunks on one stream while a second stream runs k_col_pass over
-// every chunk that has landed (the VALIDATE range check and the in-degree count
-// R34's hub tags need), so both hide under the copy.  A whole-graph copy
-// (col_bound == n, m > 0) leaves the in-degrees in g->d_indeg for the tagging.
+// L2 set-aside for evict_last (persisting) lines: the per-vertex state the
+// edge loop hits at random (BFS dist, PR residue) is accessed with an
+// evict_last policy, which only persists within this carve-out (default 0;
+// measured 51% atomic misses on a 64 MB residue array without it).
+static void l2_carveout(int device) {
+  int max_persist = 0;
+  if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess &&
+      max_persist > 0) {
+    size_t cur = 0;
+    if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < (size_t)max_persist)
+      (void)cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+    (void)cudaGetLastError();
+  }
+}
+
+// Upload of a library-owned CSR copy, then ONE pass over the columns
+// (k_col_pass): the VALIDATE range check fused with the in-degree count R34's
+// hub tags need.  A whole-graph copy (col_bound == n, m > 0) leaves the
+// in-degrees in g->d_indeg for the tagging.  (A pipelined variant — columns in
+// 128 MB chunks on a second stream with the pass over each landed chunk —
+// made create 2-3 ms shorter but the PageRank kernel that later runs on the
+// uploaded graph 2.3% slower, 160.5 -> 164.1 ms, in same-box A/B runs, so it
+// was dropped: profiles/r02_e2e_breakdown.md.)
 static atos_status upload_csr(atos_graph g, const int64_t* off, const int32_t* col, bool dev_ptrs,
                               int64_t col_bound, bool validate) {
   const int64_t n = g->n, m = g->m;
@@ -285,38 +303,13 @@ static atos_status upload_csr(atos_graph g, const int64_t* off, const int32_t* c
     CK(pool_malloc(&g->d_indeg, (size_t)n * sizeof(uint32_t)));
     CK(cudaMemset(g->d_indeg, 0, (size_t)n * sizeof(uint32_t)));
   }
-  CK(cudaDeviceSynchronize());  // the allocations and zeroing above ran on the legacy stream
-  cudaStream_t cp = nullptr, pass = nullptr;
-  cudaEvent_t landed = nullptr;
-  auto done = [&](cudaError_t e) {
-    if (cp) cudaStreamSynchronize(cp);
-    if (pass) cudaStreamSynchronize(pass);
-    if (landed) cudaEventDestroy(landed);
-    if (cp) cudaStreamDestroy(cp);
-    if (pass) cudaStreamDestroy(pass);
-    if (e != cudaSuccess) return atos_set_error(ATOS_ERR_CUDA, "CSR upload: %s", cudaGetErrorString(e));
-    return ATOS_OK;
-  };
-  cudaError_t e = cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pass, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&landed, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_off, off, (size_t)(n + 1) * sizeof(int64_t), kind, cp);
-  unsigned int* bad = validate ? reinterpret_cast<unsigned int*>(g->d_scratch) : nullptr;
-  uint32_t* indeg = count ? g->d_indeg : nullptr;
-  const int64_t chunk = (int64_t)1 << 25;  // 128 MB of columns
-  for (int64_t e0 = 0; e == cudaSuccess && e0 < m; e0 += chunk) {
-    const int64_t e1 = std::min(m, e0 + chunk);
-    e = cudaMemcpyAsync(g->d_col + e0, col + e0, (size_t)(e1 - e0) * sizeof(int32_t), kind, cp);
-    if (e == cudaSuccess && (bad || indeg)) {
-      e = cudaEventRecord(landed, cp);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(pass, landed, 0);
-      if (e == cudaSuccess) {
-        k_col_pass<<<grid_for(e1 - e0, 256, g->sms), 256, 0, pass>>>(g->d_col, e0, e1, n, col_bound, indeg, bad);
-        e = cudaGetLastError();
-      }
-    }
-  }
-  return done(e);
+  CK(cudaMemcpy(g->d_off, off, (size_t)(n + 1) * sizeof(int64_t), kind));
+  if (m) CK(cudaMemcpy(g->d_col, col, (size_t)m * sizeof(int32_t), kind));
+  if (m && (validate || count))
+    k_col_pass<<<grid_for(m, 256, g->sms), 256>>>(g->d_col, 0, m, n, col_bound, count ? g->d_indeg : nullptr,
+                                                  validate ? reinterpret_cast<unsigned int*>(g->d_scratch) : nullptr);
+  CK(cudaGetLastError());
+  return ATOS_OK;
 }
 
 atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* col, int64_t n, int64_t m,
@@ -342,20 +335,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     g->owned = true;
     CKS(upload_csr(g, off, col, dev_ptrs, col_bound, (flags & ATOS_GRAPH_VALIDATE) != 0));
   }
-  // L2 set-aside for evict_last (persisting) lines: the per-vertex state the
-  // edge loop hits at random (BFS dist, PR residue) is accessed with an
-  // evict_last policy, which only persists within this carve-out (default 0;
-  // measured 51% atomic misses on a 64 MB residue array without it).
-  {
-    int max_persist = 0;
-    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device) == cudaSuccess &&
-        max_persist > 0) {
-      size_t cur = 0;
-      if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < (size_t)max_persist)
-        (void)cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
-      (void)cudaGetLastError();
-    }
-  }
+  l2_carveout(g->device);
   if (!g->d_scratch) {
     CK(cudaMalloc(&g->d_scratch, 256));
     CK(cudaMemset(g->d_scratch, 0, 256));
@@ -376,7 +356,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
   CK(cudaMemcpy(&hmd, md, sizeof hmd, cudaMemcpyDeviceToHost));
   g->max_degree = (int64_t)hmd;
   // dangling-vertex bitmap (R29): a property of the immutable CSR, like the max degree
-  CK(pool_malloc(&g->d_sink, (size_t)std::max<int64_t>(1, (n + 31) / 32) * sizeof(uint32_t)));
+  if (!g->d_sink) CK(pool_malloc(&g->d_sink, (size_t)std::max<int64_t>(1, (n + 31) / 32) * sizeof(uint32_t)));
   if (n) k_sink_bitmap<<<grid_for(n, 256, g->sms), 256>>>(g->d_off, n, g->d_sink);
   // Hub tags (R34): a library-owned CSR of a whole graph gets bit 31 set on
   // every column entry whose target has in-degree >= HUB_IN_DEG, plus a hub
@@ -387,7 +367,7 @@ atos_status graph_init_common(atos_graph g, const int64_t* off, const int32_t* c
     g->d_indeg = nullptr;
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g->d_scratch) + 4;
     CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
-    CK(pool_malloc(&g->d_hub, (size_t)((n + 31) / 32) * sizeof(uint32_t)));
+    if (!g->d_hub) CK(pool_malloc(&g->d_hub, (size_t)((n + 31) / 32) * sizeof(uint32_t)));
     k_hub_bitmap<<<grid_for(n, 256, g->sms), 256>>>(indeg, n, HUB_IN_DEG, g->d_hub, cnt);
     unsigned long long hubs = 0;
     CK(cudaMemcpy(&hubs, cnt, sizeof hubs, cudaMemcpyDeviceToHost));
