@@ -8,11 +8,13 @@
 //   atom   returning f32 atomicAdd on every target (the threshold-crossing push)
 //   red    red.add.f32 on every target
 //   mixed  red.add.f64 for targets whose column carries HUB_TAG (bit 31; in-degree
-//          >= 512, R34/R35) and returning f32 atomicAdd for the others — the
-//          product's R35 push
+//          >= the threshold tools/atomic_trace.py tags with, 2048 in the product,
+//          R34/R35) and returning f32 atomicAdd for the others
 //   mixed, R replicas  the same with each hub's fp64 residue spread over R
-//          arrays n elements apart (replica = lane bits): what splitting a hub's
-//          residue would buy against hot-line contention
+//          arrays n elements apart (replica = lane bits); R = 4 is the product's
+//          push (R38)
+//   mode 6  4 hub replicas and the non-hub returning atomics over 2 fp32
+//          arrays (measured worse: the non-hub lines are not contended)
 // Input: a raw int32 file of column entries (tools/atomic_trace.py writes it).
 // Prints G ops/s per mode.  Not part of the product.
 #include <cstdint>
